@@ -54,6 +54,9 @@ def _load():
                                              i64p, ctypes.c_int64, u64p, ctypes.c_int]
         lib.oracle_polymul_coeffs.argtypes = [ctypes.c_uint64, u64p, ctypes.c_int64, u64p, ctypes.c_int64,
                                               i64p, ctypes.c_int64, u64p, ctypes.c_int]
+        lib.oracle_poly_eval.argtypes = [ctypes.c_uint64, u64p, ctypes.c_int64, u64p, ctypes.c_int64, u64p,
+                                         ctypes.c_int]
+        lib.oracle_poly_eval.restype = ctypes.c_int
         lib.oracle_bigint_mul.argtypes = [u32p, ctypes.c_int64, u32p, ctypes.c_int64, u32p]
         lib.oracle_bigint_mul_school.argtypes = [u32p, ctypes.c_int64, u32p, ctypes.c_int64, u32p]
         for fn in (lib.oracle_fcirc_entries, lib.oracle_polymul_coeffs, lib.oracle_bigint_mul,
@@ -110,6 +113,41 @@ def polymul_coeffs(p: int, a, b, ks=None, threads: int | None = None) -> np.ndar
     if rc != 0:
         raise ValueError("oracle_polymul_coeffs: bad arguments")
     return out
+
+
+def poly_eval(p: int, c, xs, threads: int | None = None) -> np.ndarray:
+    """sum_i c_i x^i mod p for each x in xs (Horner's rule).  Used for the eigen-checksum
+     and Schwartz-Zippel checks of whole outputs."""
+    lib = _load()
+    c = np.ascontiguousarray(np.asarray(c, dtype=np.uint64))
+    xs = np.ascontiguousarray(np.asarray([int(x) % int(p) for x in xs], dtype=np.uint64))
+    out = np.zeros(xs.shape[0], dtype=np.uint64)
+    rc = lib.oracle_poly_eval(int(p), _ptr(c, ctypes.c_uint64), c.shape[0], _ptr(xs, ctypes.c_uint64), xs.shape[0],
+                              _ptr(out, ctypes.c_uint64), threads or default_threads())
+    if rc != 0:
+        raise ValueError("oracle_poly_eval: bad arguments")
+    return out
+
+
+def eigen_thetas(p: int, n: int, w: int, count: int, seed: int) -> list[int]:
+    """``count`` seeded theta with theta^n f = 1 for f = w^n: theta = w^-1 zeta_n^e."""
+    import random as _random
+    g = {998244353: 3, 469762049: 3, 167772161: 3, (1 << 64) - (1 << 32) + 1: 7}[int(p)]
+    z = pow(g, (p - 1) // n, p)
+    winv = pow(int(w), -1, p)
+    rng = _random.Random(seed)
+    return [winv * pow(z, rng.randrange(n), p) % p for _ in range(count)]
+
+
+def eigen_check(p: int, n: int, f: int, a, b, c, thetas) -> bool:
+    """sum_i c_i theta^i == (sum_j b_j theta^j)(sum_k a_k theta^-k) for every theta (theta^n f = 1)."""
+    for th in thetas:
+        assert pow(th, n, p) * f % p == 1
+    thi = [pow(int(t), -1, p) for t in thetas]
+    lhs = poly_eval(p, c, thetas)
+    eb = poly_eval(p, b, thetas)
+    ea = poly_eval(p, a, thi)
+    return all(int(l) == int(x) * int(y) % p for l, x, y in zip(lhs, eb, ea))
 
 
 def bigint_mul(x, y, school: bool = False) -> np.ndarray:

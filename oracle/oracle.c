@@ -16,6 +16,8 @@
  *                          so the oracle is this definition, NOT Algorithm 1.  O(n) per entry.
  *   oracle_polymul_coeffs  the product of two polynomials: schoolbook coefficient
  *                            C_k = sum_{i} a_i b_{k-i} (mod p).  O(n) per coefficient.
+ *   oracle_poly_eval       sum_i c_i x^i mod p by Horner's rule (used for the eigen-checksum of
+ *                          SURVEY App. B.4 and Schwartz-Zippel checks; a plain definition).
  *   oracle_bigint_mul      product of two non-negative integers given as little-endian 32-bit
  *                          words (P:135-140 application): an independent Karatsuba recursion
  *                          (schoolbook below 32 words).  Exact, full product.
@@ -142,6 +144,36 @@ int oracle_polymul_coeffs(uint64_t p, const uint64_t* a, int64_t na, const uint6
   for (int64_t t = 0; t < nk; ++t) if (ks[t] < 0 || ks[t] >= na + nb - 1) return -1;
   job_t J = {1, p, 0, a, b, 0, na, nb, ks, out, 0, 0};
   return run_jobs(J, nk, threads);
+}
+
+/* out[t] = sum_{i<n} c_i xs[t]^i mod p (Horner, one reduction per step), for nx points */
+typedef struct { uint64_t p; const uint64_t* c; int64_t n; const uint64_t* xs; uint64_t* out; int64_t lo, hi; } ejob_t;
+static void* eval_worker(void* arg) {
+  ejob_t* J = (ejob_t*)arg;
+  for (int64_t t = J->lo; t < J->hi; ++t) {
+    u128 acc = 0, x = J->xs[t] % J->p;
+    for (int64_t i = J->n - 1; i >= 0; --i) acc = (acc * x + J->c[i]) % J->p;
+    J->out[t] = (uint64_t)acc;
+  }
+  return NULL;
+}
+int oracle_poly_eval(uint64_t p, const uint64_t* c, int64_t n, const uint64_t* xs, int64_t nx, uint64_t* out,
+                     int threads) {
+  if (!c || !xs || !out || n < 1 || nx < 0 || p < 2) return -1;
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  if (nx < threads) threads = nx > 0 ? (int)nx : 1;
+  pthread_t th[256]; ejob_t jobs[256]; int made[256];
+  for (int t = 0; t < threads; ++t) {
+    ejob_t J = {p, c, n, xs, out, nx * t / threads, nx * (t + 1) / threads};
+    jobs[t] = J;
+  }
+  for (int t = 0; t < threads; ++t) {
+    made[t] = threads > 1 && pthread_create(&th[t], NULL, eval_worker, &jobs[t]) == 0;
+    if (!made[t]) eval_worker(&jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) if (made[t]) pthread_join(th[t], NULL);
+  return 0;
 }
 
 /* ---------------- big integers: independent Karatsuba on 32-bit words ---------------- */

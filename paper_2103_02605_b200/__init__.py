@@ -1,0 +1,215 @@
+"""paper_2103_02605_b200 — thin Python binding of libfcirc (include/fcirc.h).
+
+Argument marshalling only: every step of the f-circulant product (arXiv 2103.02605, Theorem 1 /
+Algorithm 1) runs in the sm_100a kernels of ``lib/libfcirc.so``.  PyTorch is used for
+device memory and streams.  There is no CPU fallback: if the library is missing this module raises.
+
+Functions mirror the C ABI names:
+  matvec(a, b, f, p, out=None)      -> fcirc_matvec       (device tensors [batch, n])
+  matvec_host(a, b, f, p, out=None) -> fcirc_matvec_host  (host arrays/tensors, pinned preferred)
+  polymul(a, b, p, out=None)        -> fcirc_polymul      (device tensors [batch, na], [batch, nb])
+  bigint_mul(x, y, out=None)        -> bigint_mul         (device uint32 words [batch, nx], [batch, ny])
+  plan_table(p, f, n)               -> fcirc_plan_table   (host-only twist-table inspection)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+__all__ = ["FcircError", "matvec", "matvec_host", "polymul", "bigint_mul", "plan_table", "strerror",
+           "last_launch_count", "release_cache", "version", "library_path", "P998", "P469", "P167",
+           "GOLDILOCKS", "PRIMES"]
+
+P998 = 998244353
+P469 = 469762049
+P167 = 167772161
+GOLDILOCKS = (1 << 64) - (1 << 32) + 1
+PRIMES = (P998, P469, P167, GOLDILOCKS)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "lib", "libfcirc.so")
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+class FcircError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        super().__init__(f"{where}: {strerror(code)} (status {code})")
+
+
+def _load():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise RuntimeError(f"libfcirc.so not built at {_LIB_PATH}; run `python __graft_entry__.py build` "
+                           "(no CPU fallback exists)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    u64, i64, vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p
+    lib.fcirc_matvec.argtypes = [u64, u64, vp, vp, vp, i64, i64, vp]
+    lib.fcirc_matvec_host.argtypes = [u64, u64, vp, vp, vp, i64, i64]
+    lib.fcirc_polymul.argtypes = [u64, vp, i64, vp, i64, vp, i64, vp]
+    lib.bigint_mul.argtypes = [vp, i64, vp, i64, vp, i64, vp]
+    lib.fcirc_plan_table.argtypes = [u64, u64, i64, vp, vp, ctypes.POINTER(u64), ctypes.POINTER(u64)]
+    for fn in (lib.fcirc_matvec, lib.fcirc_matvec_host, lib.fcirc_polymul, lib.bigint_mul, lib.fcirc_plan_table,
+               lib.fcirc_release_cache):
+        fn.restype = ctypes.c_int
+    lib.fcirc_strerror.argtypes = [ctypes.c_int]
+    lib.fcirc_strerror.restype = ctypes.c_char_p
+    lib.fcirc_version.restype = ctypes.c_char_p
+    lib.fcirc_last_launch_count.restype = i64
+    _lib = lib
+    return lib
+
+
+def strerror(code: int) -> str:
+    return _load().fcirc_strerror(int(code)).decode()
+
+
+def version() -> str:
+    return _load().fcirc_version().decode()
+
+
+def last_launch_count() -> int:
+    return int(_load().fcirc_last_launch_count())
+
+
+def release_cache() -> None:
+    _load().fcirc_release_cache()
+
+
+def _check(rc: int, where: str):
+    if rc != 0:
+        raise FcircError(rc, where)
+
+
+def _elem_bytes(p: int) -> int:
+    return 8 if int(p) >= (1 << 32) else 4
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev_tensor(x, p: int, name: str):
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if x.element_size() != _elem_bytes(p) or x.dtype.is_floating_point:
+        raise TypeError(f"{name}: element type must be a {8 * _elem_bytes(p)}-bit integer for p={p}")
+    if not x.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return x
+
+
+def _stream_handle(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def matvec(a, b, f: int, p: int, out=None, stream=None):
+    """c = A b for f-circulant A with first row ``a`` (Definition 2), batched.
+
+    ``a``, ``b``: CUDA tensors [batch, n] (or [n]) of uint32/int32 (32-bit primes) or uint64/int64
+    (Goldilocks) holding canonical residues.  Returns ``out`` (allocated if None), same shape.
+    Asynchronous on the current (or given) stream.
+    """
+    torch = _torch()
+    _dev_tensor(a, p, "a")
+    _dev_tensor(b, p, "b")
+    if a.shape != b.shape:
+        raise ValueError("a and b must have the same shape")
+    n = a.shape[-1]
+    batch = a.numel() // n if n else 0
+    if out is None:
+        out = torch.empty_like(a)
+    _dev_tensor(out, p, "out")
+    rc = _load().fcirc_matvec(int(p), int(f) % int(p), a.data_ptr(), b.data_ptr(), out.data_ptr(), n, batch,
+                              _stream_handle(stream))
+    _check(rc, "fcirc_matvec")
+    return out
+
+
+def _host_ptr(x, p: int, name: str):
+    torch = _torch()
+    if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"] or x.itemsize != _elem_bytes(p):
+            raise TypeError(f"{name}: contiguous {8 * _elem_bytes(p)}-bit integer array required")
+        return x.ctypes.data, x.shape
+    if isinstance(x, torch.Tensor) and not x.is_cuda:
+        if not x.is_contiguous() or x.element_size() != _elem_bytes(p):
+            raise TypeError(f"{name}: contiguous {8 * _elem_bytes(p)}-bit integer tensor required")
+        return x.data_ptr(), tuple(x.shape)
+    raise TypeError(f"{name} must be a host numpy array or CPU tensor")
+
+
+def matvec_host(a, b, f: int, p: int, out=None):
+    """fcirc_matvec_host: host buffers in, host buffer out (H2D, kernels, D2H pipelined)."""
+    pa, sa = _host_ptr(a, p, "a")
+    pb, sb = _host_ptr(b, p, "b")
+    if tuple(sa) != tuple(sb):
+        raise ValueError("a and b must have the same shape")
+    if out is None:
+        out = np.empty(sa, dtype=np.uint64 if _elem_bytes(p) == 8 else np.uint32)
+    pc, sc = _host_ptr(out, p, "out")
+    n = sa[-1]
+    batch = int(np.prod(sa)) // n
+    rc = _load().fcirc_matvec_host(int(p), int(f) % int(p), pa, pb, pc, n, batch)
+    _check(rc, "fcirc_matvec_host")
+    return out
+
+
+def polymul(a, b, p: int, out=None, stream=None):
+    """c = a(x) b(x) mod p for device tensors [batch, na], [batch, nb] -> [batch, na+nb-1]."""
+    torch = _torch()
+    _dev_tensor(a, p, "a")
+    _dev_tensor(b, p, "b")
+    na, nb = a.shape[-1], b.shape[-1]
+    batch = a.numel() // na
+    if b.numel() // nb != batch:
+        raise ValueError("a and b must have the same batch")
+    if out is None:
+        out = torch.empty((*a.shape[:-1], na + nb - 1), dtype=a.dtype, device=a.device)
+    _dev_tensor(out, p, "out")
+    rc = _load().fcirc_polymul(int(p), a.data_ptr(), na, b.data_ptr(), nb, out.data_ptr(), batch,
+                               _stream_handle(stream))
+    _check(rc, "fcirc_polymul")
+    return out
+
+
+def bigint_mul(x, y, out=None, stream=None):
+    """z = x * y for little-endian uint32 word tensors [batch, nx], [batch, ny] -> [batch, nx+ny]."""
+    torch = _torch()
+    _dev_tensor(x, P998, "x")
+    _dev_tensor(y, P998, "y")
+    nx, ny = x.shape[-1], y.shape[-1]
+    batch = x.numel() // nx
+    if y.numel() // ny != batch:
+        raise ValueError("x and y must have the same batch")
+    if out is None:
+        out = torch.empty((*x.shape[:-1], nx + ny), dtype=x.dtype, device=x.device)
+    _dev_tensor(out, P998, "out")
+    rc = _load().bigint_mul(x.data_ptr(), nx, y.data_ptr(), ny, out.data_ptr(), batch, _stream_handle(stream))
+    _check(rc, "bigint_mul")
+    return out
+
+
+def plan_table(p: int, f: int, n: int):
+    """Host-only: (s, sinv, w, K) of the twist table the library would use for (p, f, n)."""
+    size = max(int(n), 1)
+    s = np.zeros(size, dtype=np.uint64)
+    si = np.zeros(size, dtype=np.uint64)
+    w = ctypes.c_uint64(0)
+    K = ctypes.c_uint64(0)
+    rc = _load().fcirc_plan_table(int(p), int(f) % int(p), int(n), s.ctypes.data, si.ctypes.data,
+                                  ctypes.byref(w), ctypes.byref(K))
+    _check(rc, "fcirc_plan_table")
+    return s, si, int(w.value), int(K.value)

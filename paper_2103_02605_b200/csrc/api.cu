@@ -1,0 +1,524 @@
+// api.cu — libfcirc C ABI (include/fcirc.h): validation, plan cache, workspace, dispatch.
+//
+// Pass schedule:
+//   n <= 2^MMAX  : one k_block launch with k = 0 (fused: one HBM read of a and b, one write of c)
+//   n >  2^MMAX  : per chunk of instances sized to stay L2-resident
+//                    k_cols<fwd>  top K = L - MMAX levels of a and b  -> a' (in c), b' (workspace)
+//                    k_block      the 2^K sub-products of size 2^MMAX  -> M (in c, in place)
+//                    k_cols<inv>  top K inverse levels, 1/n scaling     -> c (in place)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "../../include/fcirc.h"
+#include "fcirc_kernels.cuh"
+#include "plan.h"
+#include "apps.cuh"
+
+namespace fcirc {
+
+static thread_local int64_t g_launches = 0;
+
+// ------------------------------------------------------------------------------------------
+// device plans
+// ------------------------------------------------------------------------------------------
+struct DevPlan {
+  HostPlan hp;
+  void* twf = nullptr;  // TwU32[n] or uint64_t[n]
+  void* twi = nullptr;
+  TwU32 last_si32{}, last_k32{};
+  uint64_t last_si64 = 0, last_k64 = 0;
+  ~DevPlan() {
+    if (twf) cudaFree(twf);
+    if (twi) cudaFree(twi);
+  }
+};
+
+static std::mutex g_mu;
+static std::mutex g_host_mu;
+static std::map<std::tuple<int, uint64_t, uint64_t, int>, std::shared_ptr<DevPlan>> g_plans;
+
+static TwU32 shoup_pair(uint64_t w, uint64_t p) {
+  TwU32 t;
+  t.w = (uint32_t)w;
+  t.q = (uint32_t)((((unsigned __int128)w) << 32) / p);
+  return t;
+}
+
+static int get_plan(int dev, uint64_t p, uint64_t f, int L, std::shared_ptr<DevPlan>* out) {
+  auto key = std::make_tuple(dev, p, f, L);
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end()) { *out = it->second; return FCIRC_OK; }
+  }
+  auto dp = std::make_shared<DevPlan>();
+  int st = build_host_plan(p, f, L, &dp->hp);
+  if (st != FCIRC_OK) return st;
+  const PrimeInfo* pi = prime_info(p);
+  const size_t n = dp->hp.s.size();
+  if (!pi->wide) {
+    std::vector<TwU32> hf(n), hi(n);
+    for (size_t i = 0; i < n; ++i) { hf[i] = shoup_pair(dp->hp.s[i], p); hi[i] = shoup_pair(dp->hp.sinv[i], p); }
+    if (cudaMalloc(&dp->twf, n * sizeof(TwU32)) != cudaSuccess) return FCIRC_ENOMEM;
+    if (cudaMalloc(&dp->twi, n * sizeof(TwU32)) != cudaSuccess) return FCIRC_ENOMEM;
+    if (cudaMemcpy(dp->twf, hf.data(), n * sizeof(TwU32), cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
+    if (cudaMemcpy(dp->twi, hi.data(), n * sizeof(TwU32), cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
+    dp->last_si32 = shoup_pair(dp->hp.last_si, p);
+    dp->last_k32 = shoup_pair(dp->hp.K, p);
+  } else {
+    if (cudaMalloc(&dp->twf, n * 8) != cudaSuccess) return FCIRC_ENOMEM;
+    if (cudaMalloc(&dp->twi, n * 8) != cudaSuccess) return FCIRC_ENOMEM;
+    if (cudaMemcpy(dp->twf, dp->hp.s.data(), n * 8, cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
+    if (cudaMemcpy(dp->twi, dp->hp.sinv.data(), n * 8, cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
+    dp->last_si64 = dp->hp.last_si;
+    dp->last_k64 = dp->hp.K;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) { *out = it->second; return FCIRC_OK; }  // another thread won
+  g_plans[key] = dp;
+  *out = dp;
+  return FCIRC_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// workspace: one grow-only device buffer per (device, stream)
+// ------------------------------------------------------------------------------------------
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+static std::map<std::tuple<int, void*, int>, Workspace> g_ws;
+
+// tag separates independent buffers of one call (0: matvec b', 1..: application scratch)
+static int get_workspace(int dev, void* stream, size_t bytes, void** out, int tag = 0) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Workspace& w = g_ws[std::make_tuple(dev, stream, tag)];
+  if (w.bytes < bytes) {
+    if (w.ptr) {
+      cudaStreamSynchronize((cudaStream_t)stream);  // previous users on this stream are done
+      cudaFree(w.ptr);
+      w.ptr = nullptr;
+      w.bytes = 0;
+    }
+    if (cudaMalloc(&w.ptr, bytes) != cudaSuccess) return FCIRC_ENOMEM;
+    w.bytes = bytes;
+  }
+  *out = w.ptr;
+  return FCIRC_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// kernel launch tables
+// ------------------------------------------------------------------------------------------
+template <class F> struct FTraits;
+template <> struct FTraits<FieldU32> { static constexpr int MMAX = 12; };
+template <> struct FTraits<FieldGold> { static constexpr int MMAX = 11; };
+constexpr int KMAX = 11;
+
+constexpr int rsel(int M) { return M < 4 ? (1 << M) : 16; }
+constexpr int ipcsel(int M) { return ((1 << M) / rsel(M)) >= 128 ? 1 : 128 / ((1 << M) / rsel(M)); }
+constexpr int wsel(int K) {
+  return (256 * rsel(K)) >> K < 8 ? 8 : ((256 * rsel(K)) >> K);
+}
+
+template <class F, int M>
+static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
+  constexpr int R = rsel(M), IPC = ipcsel(M);
+  constexpr int T = (1 << M) / R;
+  using E = typename F::T;
+  constexpr int PM = (1 << M) + ((1 << M) >> PadOf<E>::SH) + 1;
+  const size_t smem = (size_t)IPC * 2 * PM * sizeof(E);
+  auto kern = k_block<F, M, R, IPC>;
+  if (smem > 48 * 1024) {
+    static bool once = false;  // attribute set per kernel instantiation
+    if (!once) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return FCIRC_ECUDA;
+      once = true;
+    }
+  }
+  const int64_t grid = (args.units + IPC - 1) / IPC;
+  kern<<<(unsigned)grid, T * IPC, smem, st>>>(fld, args);
+  ++g_launches;
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+template <class F, int K, bool INV>
+static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
+  constexpr int R = rsel(K), W = wsel(K);
+  constexpr int threads = W * ((1 << K) / R);
+  using E = typename F::T;
+  const size_t smem = (size_t)((1 << K) + ((1 << K) >> 4)) * W * sizeof(E);
+  auto kern = k_cols<F, K, R, W, INV>;
+  if (smem > 48 * 1024) {
+    static bool once = false;
+    if (!once) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return FCIRC_ECUDA;
+      once = true;
+    }
+  }
+  args.colblocks = args.m / W;
+  args.units = instances * args.colblocks;
+  dim3 grid((unsigned)args.units, INV ? 1 : 2);
+  kern<<<grid, threads, smem, st>>>(fld, args);
+  ++g_launches;
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+template <class F, int... Ms>
+static int dispatch_block(int M, const F& fld, const BlockArgs<F>& args, cudaStream_t st,
+                          std::integer_sequence<int, Ms...>) {
+  int rc = FCIRC_EINVAL;
+  ((M == Ms ? (rc = launch_block<F, Ms>(fld, args, st), 0) : 0), ...);
+  return rc;
+}
+
+template <class F, bool INV, int... Ks>
+static int dispatch_cols(int K, const F& fld, const ColArgs<F>& args, int64_t inst, cudaStream_t st,
+                         std::integer_sequence<int, Ks...>) {
+  int rc = FCIRC_EINVAL;
+  ((K == Ks + 1 ? (rc = launch_cols<F, Ks + 1, INV>(fld, args, inst, st), 0) : 0), ...);
+  return rc;
+}
+
+static size_t chunk_bytes() {
+  static size_t v = [] {
+    const char* e = getenv("FCIRC_CHUNK_BYTES");
+    return e ? (size_t)strtoull(e, nullptr, 10) : (size_t)64 << 20;
+  }();
+  return v;
+}
+
+template <class F>
+static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
+                      int64_t batch, cudaStream_t st, int dev) {
+  using E = typename F::T;
+  using Tw = typename F::Tw;
+  constexpr int MMAX = FTraits<F>::MMAX;
+  const Tw* twf = (const Tw*)dp.twf;
+  const Tw* twi = (const Tw*)dp.twi;
+  Tw lsi, lk;
+  if constexpr (sizeof(E) == 4) { lsi = dp.last_si32; lk = dp.last_k32; }
+  else { lsi = dp.last_si64; lk = dp.last_k64; }
+  const int64_t n = (int64_t)1 << L;
+  if (L <= MMAX) {
+    BlockArgs<F> ba{(const E*)a, (const E*)b, (E*)c, batch, 0, twf, twi, lsi, lk};
+    return dispatch_block<F>(L, fld, ba, st, std::make_integer_sequence<int, MMAX + 1>{});
+  }
+  const int K = L - MMAX;
+  if (K > KMAX) return FCIRC_ESIZE;
+  const int64_t per_inst = 2 * n * (int64_t)sizeof(E);
+  int64_t C = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)chunk_bytes() / per_inst));
+  void* ws;
+  int rc = get_workspace(dev, (void*)st, (size_t)(C * n) * sizeof(E), &ws);
+  if (rc) return rc;
+  for (int64_t i0 = 0; i0 < batch; i0 += C) {
+    const int64_t cc = std::min<int64_t>(C, batch - i0);
+    const E* ai = (const E*)a + i0 * n;
+    const E* bi = (const E*)b + i0 * n;
+    E* ci = (E*)c + i0 * n;
+    E* bw = (E*)ws;
+    ColArgs<F> fa{ai, bi, ci, bw, n >> K, n, 0, 0, twf, twi, lsi, lk};
+    rc = dispatch_cols<F, false>(K, fld, fa, cc, st, std::make_integer_sequence<int, KMAX>{});
+    if (rc) return rc;
+    BlockArgs<F> ba{ci, bw, ci, cc << K, K, twf, twi, lsi, lk};
+    rc = launch_block<F, MMAX>(fld, ba, st);
+    if (rc) return rc;
+    ColArgs<F> ia{ci, nullptr, ci, nullptr, n >> K, n, 0, 0, twf, twi, lsi, lk};
+    rc = dispatch_cols<F, true>(K, fld, ia, cc, st, std::make_integer_sequence<int, KMAX>{});
+    if (rc) return rc;
+  }
+  return FCIRC_OK;
+}
+
+static FieldU32 make_u32(uint64_t p) {
+  FieldU32 fld;
+  fld.p = (uint32_t)p;
+  fld.p2 = (uint32_t)(2 * p);
+  uint32_t inv = 1;  // p^-1 mod 2^32 by Newton iteration (5 steps: 1 -> 32 correct bits)
+  for (int i = 0; i < 5; ++i) inv *= 2u - (uint32_t)p * inv;
+  fld.pinv_neg = (uint32_t)(0u - inv);
+  return fld;
+}
+
+static bool overlaps(const void* x, size_t xb, const void* y, size_t yb) {
+  const char* a0 = (const char*)x; const char* b0 = (const char*)y;
+  return a0 < b0 + yb && b0 < a0 + xb;
+}
+
+static int ilog2_exact(int64_t n) {
+  if (n < 1 || (n & (n - 1))) return -1;
+  int L = 0;
+  while (((int64_t)1 << L) < n) ++L;
+  return L;
+}
+
+// fcirc_matvec without resetting the launch counter (used by the applications as well)
+static int matvec_impl(uint64_t p, uint64_t f, const void* a, const void* b, void* c, int64_t n, int64_t batch,
+                       cudaStream_t st) {
+  if (!a || !b || !c || n < 1 || batch < 1) return FCIRC_EINVAL;
+  const int L = ilog2_exact(n);
+  if (L < 0) return FCIRC_EINVAL;
+  const PrimeInfo* pi = prime_info(p);
+  if (!pi) return FCIRC_EPRIME;
+  const size_t es = pi->wide ? 8 : 4;
+  const int maxL = pi->wide ? FTraits<FieldGold>::MMAX + KMAX : FTraits<FieldU32>::MMAX + KMAX;
+  if (L > pi->two_adicity || L > maxL) return FCIRC_ESIZE;
+  const size_t bytes = (size_t)n * (size_t)batch * es;
+  if (overlaps(c, bytes, a, bytes) || overlaps(c, bytes, b, bytes)) return FCIRC_EINVAL;
+  // Theorem 1 premises checked on the host before touching the device
+  if (f % p == 0 || powmod(f % p, (p - 1) >> L, p) != 1) return FCIRC_ENOROOT;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
+  std::shared_ptr<DevPlan> dp;
+  int rc = get_plan(dev, p, f % p, L, &dp);
+  if (rc) return rc;
+  if (pi->wide) {
+    FieldGold fld;
+    return run_matvec(fld, *dp, a, b, c, L, batch, st, dev);
+  }
+  return run_matvec(make_u32(p), *dp, a, b, c, L, batch, st, dev);
+}
+
+static int64_t next_pow2(int64_t x) {
+  int64_t r = 1;
+  while (r < x) r <<= 1;
+  return r;
+}
+
+// polynomial product through an f = 1 circulant of order L; a~ embedding (R8)
+template <class E>
+static int polymul_impl(uint64_t p, const E* a, int64_t na, const E* b, int64_t nb, E* c, int64_t batch,
+                        cudaStream_t st, int tag) {
+  const int64_t nc = na + nb - 1;
+  const int64_t L = next_pow2(nc);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
+  void* ws;
+  int rc = get_workspace(dev, (void*)st, (size_t)(3 * batch * L) * sizeof(E), &ws, tag);
+  if (rc) return rc;
+  E* at = (E*)ws;
+  E* bp = at + batch * L;
+  E* cf = bp + batch * L;
+  const int64_t tot = batch * L;
+  const int thr = 256;
+  const int64_t blocks = std::min<int64_t>((tot + thr - 1) / thr, 148 * 16);
+  k_embed<E><<<(unsigned)blocks, thr, 0, st>>>(a, na, b, nb, at, bp, L, batch);
+  ++g_launches;
+  if (cudaPeekAtLastError() != cudaSuccess) return FCIRC_ECUDA;
+  rc = matvec_impl(p, 1, at, bp, cf, L, batch, st);
+  if (rc) return rc;
+  const int64_t totc = batch * nc;
+  const int64_t blocks2 = std::min<int64_t>((totc + thr - 1) / thr, 148 * 16);
+  k_truncate<E><<<(unsigned)blocks2, thr, 0, st>>>(cf, L, c, nc, batch);
+  ++g_launches;
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+// host buffers -> device -> host, pipelined over NSLOT streams (fcirc_matvec_host)
+struct HostCtx {
+  static constexpr int NSLOT = 3;
+  cudaStream_t st[NSLOT] = {};
+  void* buf[NSLOT] = {};
+  size_t bytes = 0;
+};
+static std::map<int, HostCtx> g_host;
+
+static int host_pipeline(uint64_t p, uint64_t f, const char* a, const char* b, char* c, int64_t n, int64_t batch,
+                         size_t es, int dev) {
+  const size_t inst_bytes = (size_t)n * es;
+  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)((size_t)32 << 20) / (int64_t)inst_bytes));
+  const size_t slot_bytes = 3 * (size_t)C * inst_bytes;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  HostCtx& hc = g_host[dev];
+  if (!hc.st[0])
+    for (int i = 0; i < HostCtx::NSLOT; ++i)
+      if (cudaStreamCreateWithFlags(&hc.st[i], cudaStreamNonBlocking) != cudaSuccess) return FCIRC_ECUDA;
+  if (hc.bytes < slot_bytes) {
+    for (int i = 0; i < HostCtx::NSLOT; ++i) {
+      cudaStreamSynchronize(hc.st[i]);
+      if (hc.buf[i]) cudaFree(hc.buf[i]);
+      hc.buf[i] = nullptr;
+    }
+    hc.bytes = 0;
+    for (int i = 0; i < HostCtx::NSLOT; ++i)
+      if (cudaMalloc(&hc.buf[i], slot_bytes) != cudaSuccess) return FCIRC_ENOMEM;
+    hc.bytes = slot_bytes;
+  }
+  int rc = FCIRC_OK;
+  int64_t chunk = 0;
+  for (int64_t i0 = 0; i0 < batch && rc == FCIRC_OK; i0 += C, ++chunk) {
+    const int64_t cc = std::min<int64_t>(C, batch - i0);
+    const int sl = (int)(chunk % HostCtx::NSLOT);
+    cudaStream_t st = hc.st[sl];
+    char* dA = (char*)hc.buf[sl];
+    char* dB = dA + (size_t)C * inst_bytes;
+    char* dC = dB + (size_t)C * inst_bytes;
+    const size_t off = (size_t)i0 * inst_bytes, nb = (size_t)cc * inst_bytes;
+    if (cudaMemcpyAsync(dA, a + off, nb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpyAsync(dB, b + off, nb, cudaMemcpyHostToDevice, st) != cudaSuccess) { rc = FCIRC_ECUDA; break; }
+    rc = matvec_impl(p, f, dA, dB, dC, n, cc, st);
+    if (rc) break;
+    if (cudaMemcpyAsync(c + off, dC, nb, cudaMemcpyDeviceToHost, st) != cudaSuccess) rc = FCIRC_ECUDA;
+  }
+  for (int i = 0; i < HostCtx::NSLOT; ++i)
+    if (cudaStreamSynchronize(hc.st[i]) != cudaSuccess && rc == FCIRC_OK) rc = FCIRC_ECUDA;
+  return rc;
+}
+
+// big-integer product (reading R12)
+static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t ny, uint32_t* z, int64_t batch,
+                       cudaStream_t st) {
+  const uint64_t P1 = 998244353ull, P2 = 469762049ull, P3 = 167772161ull;
+  const int64_t nd = 2 * (nx + ny), ncoef = nd - 1;
+  const int64_t L = next_pow2(ncoef);
+  if (ilog2_exact(L) > 23) return FCIRC_ESIZE;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
+  const size_t need = (size_t)(5 * batch * L) * 4 + (size_t)(2 * batch * ncoef) * 8 + (size_t)(batch * nd) * 4;
+  void* ws;
+  int rc = get_workspace(dev, (void*)st, need, &ws, 2);
+  if (rc) return rc;
+  uint32_t* at = (uint32_t*)ws;
+  uint32_t* bp = at + batch * L;
+  uint32_t* r1 = bp + batch * L;
+  uint32_t* r2 = r1 + batch * L;
+  uint32_t* r3 = r2 + batch * L;
+  uint64_t* V = (uint64_t*)(r3 + batch * L);
+  uint32_t* E = (uint32_t*)(V + 2 * batch * ncoef);
+  const int thr = 256;
+  auto nblk = [&](int64_t tot) { return (unsigned)std::min<int64_t>((tot + thr - 1) / thr, 148 * 16); };
+  k_bigint_embed<<<nblk(batch * L), thr, 0, st>>>(x, nx, y, ny, at, bp, L, batch);
+  ++g_launches;
+  if (cudaPeekAtLastError() != cudaSuccess) return FCIRC_ECUDA;
+  if ((rc = matvec_impl(P1, 1, at, bp, r1, L, batch, st))) return rc;
+  if ((rc = matvec_impl(P2, 1, at, bp, r2, L, batch, st))) return rc;
+  if ((rc = matvec_impl(P3, 1, at, bp, r3, L, batch, st))) return rc;
+  GarnerConsts g;
+  g.p1 = P1; g.p2 = P2; g.p3 = P3;
+  g.inv_p1_mod_p2 = invmod(P1 % P2, P2);
+  g.p1p2_mod_p3 = mulmod(P1 % P3, P2 % P3, P3);
+  g.inv_p1p2_mod_p3 = invmod(g.p1p2_mod_p3, P3);
+  k_garner<<<nblk(batch * ncoef), thr, 0, st>>>(r1, r2, r3, L, ncoef, batch, g, V);
+  ++g_launches;
+  k_digits<<<nblk(batch * nd), thr, 0, st>>>(V, ncoef, nd, batch, E);
+  ++g_launches;
+  k_carry<<<(unsigned)batch, kCarryThreads, 0, st>>>(E, nd, z, nx + ny, nullptr);
+  ++g_launches;
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+}  // namespace fcirc
+
+using namespace fcirc;
+
+extern "C" {
+
+int bigint_mul(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t ny, uint32_t* z, int64_t batch,
+               void* stream) {
+  g_launches = 0;
+  if (!x || !y || !z || nx < 1 || ny < 1 || batch < 1) return FCIRC_EINVAL;
+  if (overlaps(z, (size_t)((nx + ny) * batch) * 4, x, (size_t)(nx * batch) * 4) ||
+      overlaps(z, (size_t)((nx + ny) * batch) * 4, y, (size_t)(ny * batch) * 4))
+    return FCIRC_EINVAL;
+  return bigint_impl(x, nx, y, ny, z, batch, (cudaStream_t)stream);
+}
+
+int fcirc_matvec(uint64_t p, uint64_t f, const void* a, const void* b, void* c, int64_t n, int64_t batch,
+                 void* stream) {
+  g_launches = 0;
+  return matvec_impl(p, f, a, b, c, n, batch, (cudaStream_t)stream);
+}
+
+int fcirc_matvec_host(uint64_t p, uint64_t f, const void* a, const void* b, void* c, int64_t n,
+                      int64_t batch) {
+  g_launches = 0;
+  if (!a || !b || !c || n < 1 || batch < 1) return FCIRC_EINVAL;
+  const PrimeInfo* pi = prime_info(p);
+  if (!pi) return FCIRC_EPRIME;
+  const int L = ilog2_exact(n);
+  if (L < 0) return FCIRC_EINVAL;
+  const size_t es = pi->wide ? 8 : 4;
+  const size_t bytes = (size_t)n * (size_t)batch * es;
+  if (overlaps(c, bytes, a, bytes) || overlaps(c, bytes, b, bytes)) return FCIRC_EINVAL;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
+  return host_pipeline(p, f, (const char*)a, (const char*)b, (char*)c, n, batch, es, dev);
+}
+
+int fcirc_polymul(uint64_t p, const void* a, int64_t na, const void* b, int64_t nb, void* c, int64_t batch,
+                  void* stream) {
+  g_launches = 0;
+  if (!a || !b || !c || na < 1 || nb < 1 || batch < 1) return FCIRC_EINVAL;
+  const PrimeInfo* pi = prime_info(p);
+  if (!pi) return FCIRC_EPRIME;
+  const size_t es = pi->wide ? 8 : 4;
+  const int64_t nc = na + nb - 1;
+  if (overlaps(c, (size_t)(nc * batch) * es, a, (size_t)(na * batch) * es) ||
+      overlaps(c, (size_t)(nc * batch) * es, b, (size_t)(nb * batch) * es))
+    return FCIRC_EINVAL;
+  const int64_t L = next_pow2(nc);
+  const int maxL = pi->wide ? FTraits<FieldGold>::MMAX + KMAX : FTraits<FieldU32>::MMAX + KMAX;
+  if (ilog2_exact(L) > pi->two_adicity || ilog2_exact(L) > maxL) return FCIRC_ESIZE;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (pi->wide)
+    return polymul_impl<uint64_t>(p, (const uint64_t*)a, na, (const uint64_t*)b, nb, (uint64_t*)c, batch, st, 1);
+  return polymul_impl<uint32_t>(p, (const uint32_t*)a, na, (const uint32_t*)b, nb, (uint32_t*)c, batch, st, 1);
+}
+
+const char* fcirc_strerror(int status) {
+  switch (status) {
+    case FCIRC_OK: return "ok";
+    case FCIRC_EINVAL: return "invalid argument (null pointer, size < 1, n not a power of two, or overlap)";
+    case FCIRC_EPRIME: return "modulus not in the registry";
+    case FCIRC_ENOROOT: return "f is zero or has no n-th root mod p";
+    case FCIRC_ESIZE: return "size unsupported: no n-th root of unity mod p, or above the maximum";
+    case FCIRC_ENOMEM: return "device allocation failed";
+    case FCIRC_ECUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+int fcirc_plan_table(uint64_t p, uint64_t f, int64_t n, uint64_t* s, uint64_t* sinv, uint64_t* w, uint64_t* K) {
+  if (!s || !sinv || !w || !K) return FCIRC_EINVAL;
+  const int L = ilog2_exact(n);
+  if (L < 0) return FCIRC_EINVAL;
+  const PrimeInfo* pi = prime_info(p);
+  if (!pi) return FCIRC_EPRIME;
+  if (L > pi->two_adicity) return FCIRC_ESIZE;
+  HostPlan hp;
+  int rc = build_host_plan(p, f, L, &hp);
+  if (rc) return rc;
+  std::copy(hp.s.begin(), hp.s.end(), s);
+  std::copy(hp.sinv.begin(), hp.sinv.end(), sinv);
+  *w = hp.w;
+  *K = hp.K;
+  return FCIRC_OK;
+}
+
+const char* fcirc_version(void) { return "libfcirc 0.1 sm_100a"; }
+
+int64_t fcirc_last_launch_count(void) { return g_launches; }
+
+int fcirc_release_cache(void) {
+  cudaDeviceSynchronize();
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_plans.clear();
+  for (auto& kv : g_ws)
+    if (kv.second.ptr) cudaFree(kv.second.ptr);
+  g_ws.clear();
+  return FCIRC_OK;
+}
+
+}  // extern "C"

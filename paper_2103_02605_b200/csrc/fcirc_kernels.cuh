@@ -1,0 +1,330 @@
+// fcirc_kernels.cuh — sm_100a kernels of the f-circulant product.
+//
+// In-place iterative form of Algorithm 1 applied recursively.  The vector
+// positions of one instance are addresses 0..n-1 (L = log2 n bits).  Level d (0 <= d < L) of the
+// recursion pairs the addresses that differ in bit b = L-1-d; block e of level d holds the row of
+// an f_{d,e}-circulant and uses the twiddle s_{d,e} = sqrt(f_{d,e}); its halves become the
+// children 2e (f = +s) and 2e+1 (f = -s).  The twist table is heap-indexed: entry
+// 2^d + e, which for an element at address x is (n + x) >> (b + 1).
+//
+// Kernels:
+//   k_block   (K2 / K4) a sub-problem of size m = 2^M fully on chip: all its forward levels
+//             for a and b (sharing each twiddle load), the leaves, all its inverse levels.
+//             R elements per thread live in registers; each "phase" does r = log2 R levels in
+//             registers, phases exchange through padded shared memory.  With k = 0 it is the
+//             whole product (one HBM read of a and b, one write of c); with k > 0 it processes
+//             the 2^k independent sub-products left after the top k levels (f_{k,E}-circulants).
+//   k_cols    (K3 / K5) the top K levels, which act on columns (stride m = n / 2^K) of the
+//             instance: forward for a and b (K3), or inverse incl. the global level 0 with the
+//             1/n scaling and canonicalisation (K5).  Same register/shared-memory phase scheme
+//             along the column; W consecutive columns per CTA for coalescing.
+#pragma once
+#include <cstdint>
+#include "modarith.cuh"
+
+namespace fcirc {
+
+__host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
+
+// Phase geometry of a 2^NB-point transform done by threads holding R = 2^r points each.
+// Phase 0 covers the top r address bits, the last phase the lowest rp_last bits.
+template <int NB, int R>
+struct Phases {
+  static constexpr int r = ilog2c(R);
+  static constexpr int T = (1 << NB) / R;            // threads per transform
+  static constexpr int NPH = NB == 0 ? 0 : (NB + r - 1) / r;
+  static __host__ __device__ constexpr int rp(int ph) { return ph < NPH - 1 ? r : NB - r * (NPH - 1); }
+  static __host__ __device__ constexpr int lo(int ph) { return NB - r * ph - rp(ph); }
+  // runtime part of the address of thread t in phase ph (bits of t spread around the phase bits)
+  static __device__ __forceinline__ int ins_t(int ph, int t) {
+    const int l = lo(ph), w = rp(ph);
+    return ((t >> l) << (l + w)) | (t & ((1 << l) - 1));
+  }
+  // compile-time part of the address of slot s in phase ph
+  static __host__ __device__ constexpr int cslot(int ph, int s) {
+    const int l = lo(ph), w = rp(ph);
+    const int j = s & ((1 << w) - 1), g = s >> w;
+    const int u = g * T;  // group offset in the thread-id space
+    return ((u >> l) << (l + w)) | (j << l) | (u & ((1 << l) - 1));
+  }
+};
+
+template <class T>
+struct PadOf;
+template <>
+struct PadOf<uint32_t> { static constexpr int SH = 5; };  // one pad word per 32 words
+template <>
+struct PadOf<uint64_t> { static constexpr int SH = 4; };  // one pad element per 16 elements
+
+template <class T>
+__device__ __forceinline__ int padi(int x) { return x + (x >> PadOf<T>::SH); }
+
+// ------------------------------------------------------------------------------------------
+// k_block: fused sub-problem kernel
+// ------------------------------------------------------------------------------------------
+template <class F>
+struct BlockArgs {
+  const typename F::T* a;   // a' (row, after the top k levels), [units][m]
+  const typename F::T* b;   // b'
+  typename F::T* out;       // M (k > 0) or c (k == 0); may alias a
+  int64_t units;            // batch * 2^k
+  int k;                    // levels above this kernel (0: whole problem)
+  const typename F::Tw* twf;  // heap-indexed s_{d,e}
+  const typename F::Tw* twi;  // heap-indexed s_{d,e}^-1
+  typename F::Tw last_si;   // s_{0,0}^-1 * K   (used when k == 0)
+  typename F::Tw last_k;    // K = n^-1 (x R for FieldU32)
+};
+
+template <class F, int M, int R, int IPC>
+__global__ void __launch_bounds__((1 << M) / R * IPC)
+k_block(F fld, BlockArgs<F> args) {
+  using T = typename F::T;
+  using Tw = typename F::Tw;
+  using PH = Phases<M, R>;
+  constexpr int m = 1 << M;
+  constexpr int TT = PH::T;
+  constexpr int NPH = PH::NPH;
+  constexpr int PM = m + (m >> PadOf<T>::SH) + 1;  // padded length of one array in smem
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+
+  const int t = threadIdx.x % TT;
+  const int li = threadIdx.x / TT;
+  const int64_t unit = (int64_t)blockIdx.x * IPC + li;
+  const bool active = unit < args.units;
+  T* sa = sm + (size_t)li * 2 * PM;
+  T* sb = sa + PM;
+
+  const int k = args.k;
+  const int E = (int)(unit & ((1 << k) - 1));
+  const int gbase = ((1 << k) + E) << M;   // heap-extended address base (fits: < 2n <= 2^24)
+  const int64_t base = unit * m;
+
+  T xa[R], xb[R];
+  // ---- load (phase-0 addresses: slot s at s * 2^lo + t, coalesced across t)
+  if (active) {
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
+      xa[s] = args.a[base + ad];
+      xb[s] = args.b[base + ad];
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < R; ++s) { xa[s] = 0; xb[s] = 0; }
+  }
+
+  // ---- forward levels (Algorithm 1 split of a and b), phase by phase
+#pragma unroll
+  for (int ph = 0; ph < NPH; ++ph) {
+    if (ph > 0) {
+      const int wb = PH::ins_t(ph - 1, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int ad = padi<T>(wb) + padi<T>(PH::cslot(ph - 1, s));
+        sa[ad] = xa[s];
+        sb[ad] = xb[s];
+      }
+      __syncthreads();
+      const int rb = PH::ins_t(ph, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int ad = padi<T>(rb) + padi<T>(PH::cslot(ph, s));
+        xa[s] = sa[ad];
+        xb[s] = sb[ad];
+      }
+      __syncthreads();
+    }
+    const int rp = PH::rp(ph), lo = PH::lo(ph);
+    const int tb = gbase | PH::ins_t(ph, t);
+#pragma unroll
+    for (int l = 0; l < rp; ++l) {
+      const int jb = rp - 1 - l;
+      const int bbit = lo + jb;
+      const int tsh = tb >> (bbit + 1);
+#pragma unroll
+      for (int s0 = 0; s0 < R; ++s0) {
+        if ((s0 >> jb) & 1) continue;
+        const int s1 = s0 + (1 << jb);
+        const Tw tw = args.twf[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+        fld.fwd_a(xa[s0], xa[s1], tw);
+        fld.fwd_b(xb[s0], xb[s1], tw);
+      }
+    }
+  }
+
+  // ---- leaves: 1x1 products (the recursion bottom), same thread/slot layout
+  if constexpr (M == 0) {
+    if (active) args.out[base] = fld.single(xa[0], xb[0], args.last_k);
+    return;
+  } else {
+  T xm[R];
+#pragma unroll
+  for (int s = 0; s < R; ++s) xm[s] = fld.leaf(xa[s], xb[s]);
+
+  // ---- inverse levels (recombination c1 = (M1+M2)/(2s), c2 = (M1-M2)/2), low bits first
+  const bool top = (k == 0);
+#pragma unroll
+  for (int ph = NPH - 1; ph >= 0; --ph) {
+    if (ph < NPH - 1) {
+      const int wb = PH::ins_t(ph + 1, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) sa[padi<T>(wb) + padi<T>(PH::cslot(ph + 1, s))] = xm[s];
+      __syncthreads();
+      const int rb = PH::ins_t(ph, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) xm[s] = sa[padi<T>(rb) + padi<T>(PH::cslot(ph, s))];
+      __syncthreads();
+    }
+    const int rp = PH::rp(ph), lo = PH::lo(ph);
+    const int tb = gbase | PH::ins_t(ph, t);
+#pragma unroll
+    for (int l = 0; l < rp; ++l) {
+      const int jb = l;
+      const int bbit = lo + jb;
+      const int tsh = tb >> (bbit + 1);
+#pragma unroll
+      for (int s0 = 0; s0 < R; ++s0) {
+        if ((s0 >> jb) & 1) continue;
+        const int s1 = s0 + (1 << jb);
+        if (bbit == M - 1 && top) {
+          fld.inv_last(xm[s0], xm[s1], args.last_si, args.last_k);
+        } else {
+          const Tw tw = args.twi[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+          fld.inv(xm[s0], xm[s1], tw);
+        }
+      }
+    }
+  }
+
+  // ---- store (phase-0 addresses, coalesced)
+  if (active) {
+#pragma unroll
+    for (int s = 0; s < R; ++s) args.out[base + PH::ins_t(0, t) + PH::cslot(0, s)] = xm[s];
+  }
+  }  // M > 0
+}
+
+// ------------------------------------------------------------------------------------------
+// k_cols: the top K levels, along columns of stride m = n / 2^K
+// ------------------------------------------------------------------------------------------
+template <class F>
+struct ColArgs {
+  const typename F::T* src0;  // forward: a      inverse: M
+  const typename F::T* src1;  // forward: b      inverse: unused
+  typename F::T* dst0;        // forward: a'     inverse: c (may alias src0)
+  typename F::T* dst1;        // forward: b'
+  int64_t m;                  // column stride = n >> K
+  int64_t n;
+  int64_t colblocks;          // m / W
+  int64_t units;              // instances * colblocks
+  const typename F::Tw* twf;
+  const typename F::Tw* twi;
+  typename F::Tw last_si;
+  typename F::Tw last_k;
+};
+
+template <class F, int K, int R, int W, bool INV>
+__global__ void __launch_bounds__(W * ((1 << K) / R))
+k_cols(F fld, ColArgs<F> args) {
+  using T = typename F::T;
+  using Tw = typename F::Tw;
+  using PH = Phases<K, R>;
+  constexpr int NPH = PH::NPH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sm = reinterpret_cast<T*>(smem_raw);
+
+  const int c = threadIdx.x % W;
+  const int t = threadIdx.x / W;
+  const int64_t unit = blockIdx.x;
+  const int64_t inst = unit / args.colblocks;
+  const int64_t cb = unit - inst * args.colblocks;
+  const int64_t base = inst * args.n + cb * W + c;
+  const int64_t m = args.m;
+  const bool second = (!INV) && blockIdx.y == 1;   // forward: y = 0 -> a, y = 1 -> b
+  const T* src = second ? args.src1 : args.src0;
+  T* dst = second ? args.dst1 : args.dst0;
+
+  auto sidx = [&](int row) { return (row + (row >> 4)) * W + c; };
+
+  T x[R];
+  const int ph_first = INV ? NPH - 1 : 0;
+  {
+    const int rb = PH::ins_t(ph_first, t);
+#pragma unroll
+    for (int s = 0; s < R; ++s) x[s] = src[base + (int64_t)(rb + PH::cslot(ph_first, s)) * m];
+  }
+
+  if (!INV) {
+#pragma unroll
+    for (int ph = 0; ph < NPH; ++ph) {
+      if (ph > 0) {
+        const int wb = PH::ins_t(ph - 1, t);
+#pragma unroll
+        for (int s = 0; s < R; ++s) sm[sidx(wb + PH::cslot(ph - 1, s))] = x[s];
+        __syncthreads();
+        const int rb = PH::ins_t(ph, t);
+#pragma unroll
+        for (int s = 0; s < R; ++s) x[s] = sm[sidx(rb + PH::cslot(ph, s))];
+        __syncthreads();
+      }
+      const int rp = PH::rp(ph), lo = PH::lo(ph);
+      const int tb = (1 << K) | PH::ins_t(ph, t);
+#pragma unroll
+      for (int l = 0; l < rp; ++l) {
+        const int jb = rp - 1 - l;
+        const int bbit = lo + jb;
+        const int tsh = tb >> (bbit + 1);
+#pragma unroll
+        for (int s0 = 0; s0 < R; ++s0) {
+          if ((s0 >> jb) & 1) continue;
+          const int s1 = s0 + (1 << jb);
+          const Tw tw = args.twf[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+          if (second) fld.fwd_b(x[s0], x[s1], tw);
+          else fld.fwd_a(x[s0], x[s1], tw);
+        }
+      }
+    }
+    const int rb = PH::ins_t(NPH - 1, t);
+#pragma unroll
+    for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(NPH - 1, s)) * m] = x[s];
+  } else {
+#pragma unroll
+    for (int ph = NPH - 1; ph >= 0; --ph) {
+      if (ph < NPH - 1) {
+        const int wb = PH::ins_t(ph + 1, t);
+#pragma unroll
+        for (int s = 0; s < R; ++s) sm[sidx(wb + PH::cslot(ph + 1, s))] = x[s];
+        __syncthreads();
+        const int rb = PH::ins_t(ph, t);
+#pragma unroll
+        for (int s = 0; s < R; ++s) x[s] = sm[sidx(rb + PH::cslot(ph, s))];
+        __syncthreads();
+      }
+      const int rp = PH::rp(ph), lo = PH::lo(ph);
+      const int tb = (1 << K) | PH::ins_t(ph, t);
+#pragma unroll
+      for (int l = 0; l < rp; ++l) {
+        const int jb = l;
+        const int bbit = lo + jb;
+        const int tsh = tb >> (bbit + 1);
+#pragma unroll
+        for (int s0 = 0; s0 < R; ++s0) {
+          if ((s0 >> jb) & 1) continue;
+          const int s1 = s0 + (1 << jb);
+          if (bbit == K - 1) {
+            fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
+          } else {
+            const Tw tw = args.twi[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+            fld.inv(x[s0], x[s1], tw);
+          }
+        }
+      }
+    }
+    const int rb = PH::ins_t(0, t);
+#pragma unroll
+    for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(0, s)) * m] = x[s];
+  }
+}
+
+}  // namespace fcirc

@@ -325,3 +325,30 @@ def test_oracle_header_says_test_infrastructure():
     for name in ("__init__.py", "oracle.c"):
         with open(os.path.join(here, name)) as fh:
             assert "TEST INFRASTRUCTURE" in fh.read(4000)
+
+
+def test_poly_eval_vs_python_horner_and_closed_forms():
+    rng = random.Random(14)
+    for p in [P998, GOLDILOCKS]:
+        c = [rng.randrange(p) for _ in range(300)]
+        xs = [0, 1, p - 1, rng.randrange(p), rng.randrange(p)]
+        got = [int(v) for v in oracle.poly_eval(p, c, xs)]
+        assert got[0] == c[0]
+        assert got[1] == sum(c) % p
+        assert got[2] == sum(ci * (-1) ** i for i, ci in enumerate(c)) % p
+        for x, g in zip(xs[3:], got[3:]):
+            assert g == sum(ci * pow(x, i, p) for i, ci in enumerate(c)) % p
+
+
+def test_eigen_check_detects_a_single_corrupted_entry():
+    rng = random.Random(15)
+    p, n = P998, 64
+    w = rng.randrange(1, p)
+    f = pow(w, n, p)
+    a = [rng.randrange(p) for _ in range(n)]
+    b = [rng.randrange(p) for _ in range(n)]
+    c = [int(x) for x in oracle.fcirc_entries(p, f, a, b)]
+    th = oracle.eigen_thetas(p, n, w, 4, seed=1)
+    assert oracle.eigen_check(p, n, f, a, b, c, th)
+    c[17] = (c[17] + 1) % p
+    assert not oracle.eigen_check(p, n, f, a, b, c, th)

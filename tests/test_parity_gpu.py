@@ -1,0 +1,290 @@
+"""GPU parity: the CUDA path (through the C ABI via the thin binding) against the CPU oracle,
+element by element, bit-exact (integer work).
+
+Coverage rules:
+  * n <= 2^14: every entry of every instance (small batches; several tiles + ragged batch);
+  * n >  2^14 and BASELINE.json full sizes: >= 1024 seeded-random entries per checked instance
+    plus the boundary indices {0, 1, n/2-1, n/2, n-2, n-1}, and the eigen-checksum
+     on whole outputs;
+  * polymul: sampled coefficients + Schwartz-Zippel; bigint: the full product vs Python ints and
+    the oracle's Karatsuba.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import GOLDILOCKS, P167, P469, P998
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2103_02605_b200 as fc  # noqa: E402
+
+PRIMES = [P998, P469, P167, GOLDILOCKS]
+ADIC = {P998: 23, P469: 26, P167: 25, GOLDILOCKS: 32}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+    torch.cuda.synchronize()
+
+
+def _dev(x: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _host(t) -> np.ndarray:
+    return t.cpu().numpy()
+
+
+def run_matvec(inp):
+    a, b = _dev(inp["a"]), _dev(inp["b"])
+    c = fc.matvec(a, b, inp["f"], inp["p"])
+    torch.cuda.synchronize()
+    return _host(c)
+
+
+def check_full(inp, c, instances=None):
+    p, f = inp["p"], inp["f"]
+    for k in (range(inp["batch"]) if instances is None else instances):
+        exp = oracle.fcirc_entries(p, f, inp["a"][k], inp["b"][k])
+        got = c[k].astype(np.uint64)
+        bad = np.nonzero(got != exp)[0]
+        assert bad.size == 0, f"instance {k}: {bad.size} mismatches, first at {bad[0]}: got {got[bad[0]]} exp {exp[bad[0]]}"
+
+
+def check_sampled(inp, c, instances, count=1024, thetas=4):
+    p, f, n = inp["p"], inp["f"], inp["n"]
+    for k in instances:
+        idx = synth.sample_indices(n, count, seed=1000 + k)
+        exp = oracle.fcirc_entries(p, f, inp["a"][k], inp["b"][k], idx)
+        got = c[k][idx].astype(np.uint64)
+        bad = np.nonzero(got != exp)[0]
+        assert bad.size == 0, f"instance {k}: {bad.size} mismatches, first idx {idx[bad[0]]}"
+        if thetas and inp.get("w"):
+            th = oracle.eigen_thetas(p, n, inp["w"], thetas, seed=k)
+            assert oracle.eigen_check(p, n, f, inp["a"][k], inp["b"][k], c[k], th), f"eigen-checksum, instance {k}"
+
+
+# ---------------------------------------------------------------------------------- fused path
+
+@pytest.mark.parametrize("p", PRIMES)
+@pytest.mark.parametrize("f_mode", ["wn", "one", "minus_one"])
+def test_matvec_all_entries_small(p, f_mode):
+    """n = 2^0 .. 2^14, every entry; batch 3 (ragged against the instances-per-CTA packing)."""
+    for L in range(0, 15):
+        if f_mode == "minus_one" and L + 1 > ADIC[p]:
+            continue
+        batch = 3 if L <= 12 else 2
+        inp = synth.matvec_inputs(p, 1 << L, batch, seed=100 + L, f_mode=f_mode)
+        c = run_matvec(inp)
+        check_full(inp, c)
+
+
+@pytest.mark.parametrize("p", [P998, GOLDILOCKS])
+def test_matvec_many_instances_small_n(p):
+    """Many instances per launch (grid of several waves, ragged last CTA)."""
+    for L, batch in [(1, 1001), (4, 777), (7, 333), (10, 149)]:
+        inp = synth.matvec_inputs(p, 1 << L, batch, seed=7 + L)
+        c = run_matvec(inp)
+        check_full(inp, c, instances=[0, 1, batch // 2, batch - 2, batch - 1])
+        th_ok = all(oracle.eigen_check(p, 1 << L, inp["f"], inp["a"][k], inp["b"][k], c[k],
+                                       oracle.eigen_thetas(p, 1 << L, inp["w"], 2, seed=k)) for k in range(batch))
+        assert th_ok
+
+
+def test_matvec_extreme_values():
+    """All inputs p-1 (largest residues) and zeros, Goldilocks and 32-bit, fused and multi-pass."""
+    for p in [P998, GOLDILOCKS]:
+        for L in [3, 11, 12, 16]:
+            n = 1 << L
+            dt = np.uint64 if p == GOLDILOCKS else np.uint32
+            for val in [p - 1, 0, 1]:
+                inp = dict(p=p, n=n, batch=1, f=p - 1, w=None,
+                           a=np.full((1, n), val, dtype=dt), b=np.full((1, n), p - 1, dtype=dt))
+                c = run_matvec(inp)
+                if n <= 1 << 12:
+                    check_full(inp, c)
+                else:
+                    check_sampled(inp, c, [0], count=256, thetas=0)
+
+
+# ---------------------------------------------------------------------------------- multi-pass
+
+@pytest.mark.parametrize("p", PRIMES)
+def test_matvec_multipass_sampled(p):
+    """n = 2^13 .. 2^22 (2^23 for 998244353): three-pass schedule, sampled entries + checksum."""
+    top = 23 if p == P998 else 22
+    for L in range(13, top + 1):
+        batch = 3 if L <= 18 else 1
+        inp = synth.matvec_inputs(p, 1 << L, batch, seed=200 + L)
+        c = run_matvec(inp)
+        check_sampled(inp, c, range(batch), count=1024 if L <= 20 else 512, thetas=2)
+
+
+def test_matvec_multipass_full_entries_2pow15():
+    for p in [P998, GOLDILOCKS]:
+        inp = synth.matvec_inputs(p, 1 << 15, 2, seed=33)
+        c = run_matvec(inp)
+        check_full(inp, c)
+
+
+def test_matvec_chunking_ragged(monkeypatch):
+    """Batch not a multiple of the L2 chunk: instances in the last, short chunk are right."""
+    inp = synth.matvec_inputs(GOLDILOCKS, 1 << 16, 7, seed=44)
+    c = run_matvec(inp)
+    check_sampled(inp, c, range(7), count=256, thetas=1)
+
+
+# ---------------------------------------------------------------------------------- BASELINE configs
+
+def test_config_C1():
+    inp = synth.matvec_inputs(**{k: v for k, v in synth.CONFIGS["C1"].items() if k != "kind"})
+    c = run_matvec(inp)
+    check_full(inp, c)
+
+
+@pytest.mark.parametrize("name", ["C2_f1", "C2_fm1"])
+def test_config_C2(name):
+    cfg = {k: v for k, v in synth.CONFIGS[name].items() if k != "kind"}
+    inp = synth.matvec_inputs(**cfg)
+    c = run_matvec(inp)
+    rng = np.random.default_rng(5)
+    check_full(inp, c, instances=sorted({0, 4095, *rng.integers(0, 4096, 30).tolist()}))
+    # every instance: eigen-checksum (f = 1 -> theta^n = 1; f = -1 -> theta^n = -1)
+    p, n, f = inp["p"], inp["n"], inp["f"]
+    g = 3
+    z2n = pow(g, (p - 1) // (2 * n), p)
+    th = [1, pow(g, (p - 1) // n, p)] if f == 1 else [pow(z2n, -1, p), pow(z2n, -3, p)]
+    for k in range(inp["batch"]):
+        assert oracle.eigen_check(p, n, f, inp["a"][k], inp["b"][k], c[k], th), k
+
+
+@pytest.mark.parametrize("L", list(range(12, 23)))
+def test_config_C4_goldilocks_sweep(L):
+    cfg = {k: v for k, v in synth.CONFIGS[f"C4_n{L}"].items() if k != "kind"}
+    inp = synth.matvec_inputs(**cfg)
+    c = run_matvec(inp)
+    batch = inp["batch"]
+    ks = sorted({0, 1, batch // 2, batch - 1})
+    if L <= 14:
+        check_full(inp, c, instances=ks[:2])
+    check_sampled(inp, c, ks, count=1024, thetas=2)
+
+
+def test_config_S1():
+    cfg = {k: v for k, v in synth.CONFIGS["S1"].items() if k != "kind"}
+    inp = synth.matvec_inputs(**cfg)
+    c = run_matvec(inp)
+    check_sampled(inp, c, [0, 1, 31, 62, 63], count=1024, thetas=2)
+
+
+# ---------------------------------------------------------------------------------- host entry
+
+def test_matvec_host_matches_device():
+    for p, L, batch in [(GOLDILOCKS, 11, 5), (P998, 16, 9), (GOLDILOCKS, 20, 3)]:
+        inp = synth.matvec_inputs(p, 1 << L, batch, seed=55 + L)
+        c_host = fc.matvec_host(inp["a"], inp["b"], inp["f"], p)
+        c_dev = run_matvec(inp)
+        assert np.array_equal(c_host, c_dev)
+        check_sampled(inp, c_host, [0, batch - 1], count=256, thetas=1)
+
+
+def test_errors_through_binding():
+    a = torch.zeros((2, 16), dtype=torch.int64, device="cuda")
+    with pytest.raises(fc.FcircError) as ei:
+        fc.matvec(a, a.clone(), 7, GOLDILOCKS)  # 7 generates (Z/p)^*: not a square
+    assert ei.value.code in (-3,)
+    with pytest.raises(fc.FcircError) as ei:
+        fc.matvec(a[:, :12].contiguous(), a[:, :12].contiguous(), 1, GOLDILOCKS)
+    assert ei.value.code == -1
+    with pytest.raises(fc.FcircError) as ei:
+        fc.matvec(a, a, 1, GOLDILOCKS, out=a)
+    assert ei.value.code == -1
+
+
+def test_nondefault_stream_and_repeatability():
+    inp = synth.matvec_inputs(GOLDILOCKS, 1 << 14, 4, seed=66)
+    a, b = _dev(inp["a"]), _dev(inp["b"])
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        c1 = fc.matvec(a, b, inp["f"], GOLDILOCKS)
+        c2 = fc.matvec(a, b, inp["f"], GOLDILOCKS)
+    s.synchronize()
+    assert torch.equal(c1, c2)
+    check_sampled(inp, _host(c1), [0, 3], count=512, thetas=1)
+
+
+# ---------------------------------------------------------------------------------- polymul
+
+@pytest.mark.parametrize("p", [P998, GOLDILOCKS])
+def test_polymul_small_full(p):
+    rng = np.random.default_rng(77)
+    for na, nb, batch in [(1, 1, 2), (2, 3, 2), (17, 33, 3), (1000, 24, 2), (4096, 4096, 2), (5000, 3000, 1)]:
+        inp = synth.polymul_inputs(p, na, nb, batch, seed=int(rng.integers(1 << 30)))
+        c = fc.polymul(_dev(inp["a"]), _dev(inp["b"]), p)
+        c = _host(c)
+        for k in range(batch):
+            exp = oracle.polymul_coeffs(p, inp["a"][k], inp["b"][k])
+            assert np.array_equal(c[k].astype(np.uint64), exp), (na, nb, k)
+
+
+def test_config_C3_polymul():
+    cfg = synth.CONFIGS["C3"]
+    inp = synth.polymul_inputs(cfg["p"], cfg["na"], cfg["nb"], cfg["batch"], cfg["seed"])
+    c = _host(fc.polymul(_dev(inp["a"]), _dev(inp["b"]), cfg["p"]))
+    p, nc = cfg["p"], cfg["na"] + cfg["nb"] - 1
+    assert c.shape == (cfg["batch"], nc)
+    for k in [0, 7, 15]:
+        ks = np.unique(np.concatenate([synth.sample_indices(nc, 1024, seed=k),
+                                       [0, 1, (1 << 20) - 1, 1 << 20, nc - 1]]))
+        exp = oracle.polymul_coeffs(p, inp["a"][k], inp["b"][k], ks)
+        assert np.array_equal(c[k][ks].astype(np.uint64), exp), k
+        xs = [int(x) for x in np.random.default_rng(k).integers(1, p, 8)]
+        assert np.array_equal(oracle.poly_eval(p, c[k], xs),
+                              (oracle.poly_eval(p, inp["a"][k], xs).astype(object) *
+                               oracle.poly_eval(p, inp["b"][k], xs).astype(object) % p).astype(np.uint64))
+
+
+# ---------------------------------------------------------------------------------- bigint
+
+def _to_int(words):
+    return int.from_bytes(np.ascontiguousarray(words, dtype="<u4").tobytes(), "little")
+
+
+def test_bigint_small():
+    rng = np.random.default_rng(88)
+    for nx, ny, batch in [(1, 1, 3), (1, 5, 2), (7, 3, 2), (64, 64, 2), (1000, 777, 2), (4096, 4096, 1)]:
+        inp = synth.bigint_inputs(max(nx, ny), batch, seed=int(rng.integers(1 << 30)))
+        x = np.ascontiguousarray(inp["x"][:, :nx])
+        y = np.ascontiguousarray(inp["y"][:, :ny])
+        z = _host(fc.bigint_mul(_dev(x), _dev(y)))
+        for k in range(batch):
+            assert _to_int(z[k]) == _to_int(x[k]) * _to_int(y[k]), (nx, ny, k)
+
+
+def test_bigint_edge_values():
+    for nx in [1, 2, 33]:
+        ones = np.full((1, nx), 0xFFFFFFFF, dtype=np.uint32)
+        zeros = np.zeros((1, nx), dtype=np.uint32)
+        one = np.zeros((1, nx), dtype=np.uint32)
+        one[0, 0] = 1
+        for x, y in [(ones, ones), (zeros, ones), (one, ones)]:
+            z = _host(fc.bigint_mul(_dev(x), _dev(y)))
+            assert _to_int(z[0]) == _to_int(x[0]) * _to_int(y[0])
+    z = _host(fc.bigint_mul(_dev(np.array([[999]], dtype=np.uint32)), _dev(np.array([[999]], dtype=np.uint32))))
+    assert _to_int(z[0]) == 998001
+
+
+def test_config_C5_bigint():
+    cfg = synth.CONFIGS["C5"]
+    inp = synth.bigint_inputs(cfg["nwords"], cfg["batch"], cfg["seed"])
+    z = _host(fc.bigint_mul(_dev(inp["x"]), _dev(inp["y"])))
+    for k in range(cfg["batch"]):
+        assert _to_int(z[k]) == _to_int(inp["x"][k]) * _to_int(inp["y"][k]), k
+    # and against the oracle's independent Karatsuba, word for word
+    assert np.array_equal(z[0], oracle.bigint_mul(inp["x"][0], inp["y"][0]))
