@@ -129,6 +129,18 @@ int64_t fcirc_last_launch_count(void);
  */
 int fcirc_plan_table(uint64_t p, uint64_t f, int64_t n, uint64_t* s, uint64_t* sinv, uint64_t* w, uint64_t* K);
 
+/*
+ * Kernel-level timing (for bench.py's roofline): while enabled, every kernel launch libfcirc makes
+ * is bracketed by two CUDA events recorded on the launching stream.  fcirc_profile_read waits for
+ * the recorded events, writes per-kind launch counts and summed device milliseconds for up to
+ * `nkinds` kinds, clears the record and returns the number of kinds (FCIRC_NKINDS).
+ * Kinds: 0 k_block fused (whole problem), 1 k_block sub-problems (multi-pass), 2 k_cols forward,
+ * 3 k_cols inverse, 4 application kernels (embed/truncate/CRT/carry).
+ */
+#define FCIRC_NKINDS 5
+int fcirc_profile_enable(int on);
+int fcirc_profile_read(int64_t* counts, double* ms, int nkinds);
+
 /* release all cached plans and workspaces of the current device (for tests / teardown) */
 int fcirc_release_cache(void);
 

@@ -57,8 +57,10 @@ def _load():
     lib.fcirc_polymul.argtypes = [u64, vp, i64, vp, i64, vp, i64, vp]
     lib.bigint_mul.argtypes = [vp, i64, vp, i64, vp, i64, vp]
     lib.fcirc_plan_table.argtypes = [u64, u64, i64, vp, vp, ctypes.POINTER(u64), ctypes.POINTER(u64)]
+    lib.fcirc_profile_enable.argtypes = [ctypes.c_int]
+    lib.fcirc_profile_read.argtypes = [vp, vp, ctypes.c_int]
     for fn in (lib.fcirc_matvec, lib.fcirc_matvec_host, lib.fcirc_polymul, lib.bigint_mul, lib.fcirc_plan_table,
-               lib.fcirc_release_cache):
+               lib.fcirc_release_cache, lib.fcirc_profile_enable, lib.fcirc_profile_read):
         fn.restype = ctypes.c_int
     lib.fcirc_strerror.argtypes = [ctypes.c_int]
     lib.fcirc_strerror.restype = ctypes.c_char_p
@@ -78,6 +80,24 @@ def version() -> str:
 
 def last_launch_count() -> int:
     return int(_load().fcirc_last_launch_count())
+
+
+KERNEL_KINDS = ("k_block_fused", "k_block_sub", "k_cols_fwd", "k_cols_inv", "apps")
+
+
+def profile_enable(on: bool = True) -> None:
+    """Bracket every libfcirc launch with CUDA events on its stream (fcirc_profile_enable)."""
+    _load().fcirc_profile_enable(1 if on else 0)
+
+
+def profile_read() -> dict:
+    """{kind: (launches, device ms)} accumulated since the last read (fcirc_profile_read)."""
+    counts = np.zeros(len(KERNEL_KINDS), dtype=np.int64)
+    ms = np.zeros(len(KERNEL_KINDS), dtype=np.float64)
+    rc = _load().fcirc_profile_read(counts.ctypes.data, ms.ctypes.data, len(KERNEL_KINDS))
+    if rc < 0:
+        raise FcircError(rc, "fcirc_profile_read")
+    return {k: (int(c), float(t)) for k, c, t in zip(KERNEL_KINDS, counts, ms)}
 
 
 def release_cache() -> None:

@@ -28,6 +28,39 @@ namespace fcirc {
 static thread_local int64_t g_launches = 0;
 
 // ------------------------------------------------------------------------------------------
+// optional per-launch event timing (fcirc_profile_enable / fcirc_profile_read)
+// ------------------------------------------------------------------------------------------
+struct ProfRec { int kind; cudaEvent_t e0, e1; };
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof_recs;
+static std::vector<cudaEvent_t> g_prof_pool;
+static thread_local int t_prof_kind = -1;
+static thread_local cudaEvent_t t_prof_e0 = nullptr;
+
+static cudaEvent_t prof_event() {
+  if (!g_prof_pool.empty()) { cudaEvent_t e = g_prof_pool.back(); g_prof_pool.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+static inline void prof_begin(int kind, cudaStream_t st) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  t_prof_kind = kind;
+  t_prof_e0 = prof_event();
+  cudaEventRecord(t_prof_e0, st);
+}
+static inline void prof_end(cudaStream_t st) {
+  if (!g_prof_on || t_prof_kind < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  cudaEvent_t e1 = prof_event();
+  cudaEventRecord(e1, st);
+  g_prof_recs.push_back({t_prof_kind, t_prof_e0, e1});
+  t_prof_kind = -1;
+}
+
+// ------------------------------------------------------------------------------------------
 // device plans
 // ------------------------------------------------------------------------------------------
 struct DevPlan {
@@ -148,7 +181,9 @@ static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st)
     }
   }
   const int64_t grid = (args.units + IPC - 1) / IPC;
+  prof_begin(args.k == 0 ? 0 : 1, st);
   kern<<<(unsigned)grid, T * IPC, smem, st>>>(fld, args);
+  prof_end(st);
   ++g_launches;
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
@@ -171,7 +206,9 @@ static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStr
   args.colblocks = args.m / W;
   args.units = instances * args.colblocks;
   dim3 grid((unsigned)args.units, INV ? 1 : 2);
+  prof_begin(INV ? 3 : 2, st);
   kern<<<grid, threads, smem, st>>>(fld, args);
+  prof_end(st);
   ++g_launches;
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
@@ -314,14 +351,18 @@ static int polymul_impl(uint64_t p, const E* a, int64_t na, const E* b, int64_t 
   const int64_t tot = batch * L;
   const int thr = 256;
   const int64_t blocks = std::min<int64_t>((tot + thr - 1) / thr, 148 * 16);
+  prof_begin(4, st);
   k_embed<E><<<(unsigned)blocks, thr, 0, st>>>(a, na, b, nb, at, bp, L, batch);
+  prof_end(st);
   ++g_launches;
   if (cudaPeekAtLastError() != cudaSuccess) return FCIRC_ECUDA;
   rc = matvec_impl(p, 1, at, bp, cf, L, batch, st);
   if (rc) return rc;
   const int64_t totc = batch * nc;
   const int64_t blocks2 = std::min<int64_t>((totc + thr - 1) / thr, 148 * 16);
+  prof_begin(4, st);
   k_truncate<E><<<(unsigned)blocks2, thr, 0, st>>>(cf, L, c, nc, batch);
+  prof_end(st);
   ++g_launches;
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
@@ -399,7 +440,9 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   uint32_t* E = (uint32_t*)(V + 2 * batch * ncoef);
   const int thr = 256;
   auto nblk = [&](int64_t tot) { return (unsigned)std::min<int64_t>((tot + thr - 1) / thr, 148 * 16); };
+  prof_begin(4, st);
   k_bigint_embed<<<nblk(batch * L), thr, 0, st>>>(x, nx, y, ny, at, bp, L, batch);
+  prof_end(st);
   ++g_launches;
   if (cudaPeekAtLastError() != cudaSuccess) return FCIRC_ECUDA;
   if ((rc = matvec_impl(P1, 1, at, bp, r1, L, batch, st))) return rc;
@@ -410,11 +453,17 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   g.inv_p1_mod_p2 = invmod(P1 % P2, P2);
   g.p1p2_mod_p3 = mulmod(P1 % P3, P2 % P3, P3);
   g.inv_p1p2_mod_p3 = invmod(g.p1p2_mod_p3, P3);
+  prof_begin(4, st);
   k_garner<<<nblk(batch * ncoef), thr, 0, st>>>(r1, r2, r3, L, ncoef, batch, g, V);
+  prof_end(st);
   ++g_launches;
+  prof_begin(4, st);
   k_digits<<<nblk(batch * nd), thr, 0, st>>>(V, ncoef, nd, batch, E);
+  prof_end(st);
   ++g_launches;
+  prof_begin(4, st);
   k_carry<<<(unsigned)batch, kCarryThreads, 0, st>>>(E, nd, z, nx + ny, nullptr);
+  prof_end(st);
   ++g_launches;
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
@@ -510,6 +559,31 @@ int fcirc_plan_table(uint64_t p, uint64_t f, int64_t n, uint64_t* s, uint64_t* s
 const char* fcirc_version(void) { return "libfcirc 0.1 sm_100a"; }
 
 int64_t fcirc_last_launch_count(void) { return g_launches; }
+
+int fcirc_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+  return FCIRC_OK;
+}
+
+int fcirc_profile_read(int64_t* counts, double* ms, int nkinds) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int i = 0; i < nkinds; ++i) { if (counts) counts[i] = 0; if (ms) ms[i] = 0.0; }
+  int rc = FCIRC_NKINDS;
+  for (auto& r : g_prof_recs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.e1) != cudaSuccess || cudaEventElapsedTime(&t, r.e0, r.e1) != cudaSuccess)
+      rc = FCIRC_ECUDA;
+    if (r.kind < nkinds) {
+      if (counts) counts[r.kind] += 1;
+      if (ms) ms[r.kind] += t;
+    }
+    g_prof_pool.push_back(r.e0);
+    g_prof_pool.push_back(r.e1);
+  }
+  g_prof_recs.clear();
+  return rc;
+}
 
 int fcirc_release_cache(void) {
   cudaDeviceSynchronize();
