@@ -102,78 +102,132 @@ struct FieldGold {
   static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
   static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
 
-  // a + b mod p on weakly reduced inputs (any 64-bit values); result weakly reduced
-  __device__ __forceinline__ static uint64_t add(uint64_t a, uint64_t b) {
-    uint64_t s = a + b;
-    uint64_t c = (s < a) ? EPS : 0ull;  // wrapped: + 2^64 == + EPS
-    uint64_t t = s + c;
-    uint64_t c2 = (t < s) ? EPS : 0ull;
-    return t + c2;
-  }
-  // a - b mod p on weakly reduced inputs
-  __device__ __forceinline__ static uint64_t sub(uint64_t a, uint64_t b) {
-    uint64_t d = a - b;
-    uint64_t c = (a < b) ? EPS : 0ull;  // borrowed: - 2^64 == - EPS
-    uint64_t t = d - c;
-    uint64_t c2 = (d < c) ? EPS : 0ull;
-    return t - c2;
-  }
-  // 64 x 64 -> 128 -> mod p (weakly reduced)
-  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
-    uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32);
-    uint32_t b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
-    uint32_t t0, t1, t2, t3;
-    asm("{\n\t"
-        "mul.lo.u32      %0, %4, %6;\n\t"
-        "mul.hi.u32      %1, %4, %6;\n\t"
-        "mad.lo.cc.u32   %1, %4, %7, %1;\n\t"
-        "madc.hi.u32     %2, %4, %7, 0;\n\t"
-        "mad.lo.cc.u32   %1, %5, %6, %1;\n\t"
-        "madc.hi.cc.u32  %2, %5, %6, %2;\n\t"
-        "madc.hi.u32     %3, %5, %7, 0;\n\t"
-        "mad.lo.cc.u32   %2, %5, %7, %2;\n\t"
-        "addc.u32        %3, %3, 0;\n\t"
+  // All helpers work on 32-bit halves with explicit PTX carry chains (add.cc / addc / sub.cc /
+  // subc), so that ptxas emits IADD3 / IADD3.X with carry predicates instead of 64-bit compares
+  // and selects (profiles/r01a_ncu_full_k_block.txt: the compare/select form saturated the ALU
+  // pipe at ~53 instructions per modmul).
+  __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+  __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+  // a + b mod p for a any 64-bit value and b < p (canonical): one wrap correction suffices,
+  // since a + b - 2^64 + EPS < a + p - p <= 2^64 - 1.  Result weakly reduced.
+  __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
+    uint32_t s0, s1;
+    asm("{\n\t.reg .u32 c;\n\t.reg .pred q;\n\t"
+        "add.cc.u32  %0, %2, %4;\n\t"
+        "addc.cc.u32 %1, %3, %5;\n\t"
+        "addc.u32    c, 0, 0;\n\t"                 // carry out of 2^64
+        "setp.ne.u32 q, c, 0;\n\t"
+        "@q add.cc.u32  %0, %0, 0xffffffff;\n\t"   // + EPS
+        "@q addc.u32    %1, %1, 0;\n\t"
         "}"
-        : "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3)
-        : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
-    // t = t0 + t1 2^32 + t2 2^64 + t3 2^96 == (t1:t0) - t3 + t2 (2^32 - 1)   (mod p)
-    uint64_t lo = ((uint64_t)t1 << 32) | t0;
-    uint64_t r = lo - t3;
-    if (lo < (uint64_t)t3) r -= EPS;      // borrow: cannot borrow again (r >= 2^64 - 2^32)
-    uint64_t m = ((uint64_t)t2 << 32) - t2;  // t2 (2^32 - 1) < 2^64
-    uint64_t s = r + m;
-    if (s < m) s += EPS;                   // carry: s < m - 1 here, so s + EPS cannot wrap
-    return s;
+        : "=&r"(s0), "=&r"(s1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(s0, s1);
+  }
+  // a - b mod p for a any 64-bit value and b < p: on a borrow, a - b + 2^64 - EPS >= 2^64 - p - EPS + 1 > 0,
+  // so one correction suffices.  Result canonical if a is.
+  __device__ __forceinline__ static uint64_t sub_c(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 bw;\n\t.reg .pred q;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    bw, 0, 0;\n\t"                // -borrow
+        "setp.ne.u32 q, bw, 0;\n\t"
+        "@q sub.cc.u32  %0, %0, 0xffffffff;\n\t"   // - EPS
+        "@q subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // a - b mod p for any 64-bit a, b (two borrow corrections); result weakly reduced
+  __device__ __forceinline__ static uint64_t sub_w(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 bw;\n\t.reg .pred q;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    bw, 0, 0;\n\t"
+        "setp.ne.u32 q, bw, 0;\n\t"
+        "@q sub.cc.u32  %0, %0, 0xffffffff;\n\t"
+        "@q subc.cc.u32 %1, %1, 0;\n\t"
+        "@q subc.u32    bw, 0, 0;\n\t"             // a second borrow only if b >= p + a
+        "setp.ne.u32 q, bw, 0;\n\t"
+        "@q sub.cc.u32  %0, %0, 0xffffffff;\n\t"
+        "@q subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  //   t = t0 + t1 2^32 + t2 2^64 + t3 2^96,  2^64 == EPS, 2^96 == -1 (mod p):
+  //   s = (t1:t0) - t3            (borrow -> s -= EPS, cannot borrow again)
+  //   s = s + t2 * EPS            (carry k1)
+  //   u = s + EPS                 (carry k2: s >= p)
+  //   result = (k1 | k2) ? u : s  (k1 = 1 implies s + EPS < p; k2 = 1 means u = s - p)
+  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+    // 64x64 -> 128: ptxas expands mul.lo.u64 / mul.hi.u64 into four IMAD.WIDE.U32 with
+    // carry-in/out predicates (7 SASS instructions, measured in tools/gold_bench.cu)
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
+  //   s = (t1:t0) - t3            (borrow -> s -= EPS, cannot borrow again)
+  //   s = s + t2 * EPS            (carry k1)
+  //   u = s + EPS                 (carry k2: s >= p)
+  //   result = (k1 | k2) ? u : s  (k1 = 1 implies s + EPS < p; k2 = 1 means u = s - p)
+  __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 bw, k, u0, u1;\n\t.reg .pred q;\n\t"
+        "sub.cc.u32      %0, %2, %5;\n\t"
+        "subc.cc.u32     %1, %3, 0;\n\t"
+        "subc.u32        bw, 0, 0;\n\t"
+        "sub.cc.u32      %0, %0, bw;\n\t"
+        "subc.u32        %1, %1, 0;\n\t"
+        "mad.lo.cc.u32   %0, %4, 0xffffffff, %0;\n\t"
+        "madc.hi.cc.u32  %1, %4, 0xffffffff, %1;\n\t"
+        "addc.u32        k, 0, 0;\n\t"
+        "add.cc.u32      u0, %0, 0xffffffff;\n\t"
+        "addc.cc.u32     u1, %1, 0;\n\t"
+        "addc.u32        k, k, 0;\n\t"
+        "setp.ne.u32     q, k, 0;\n\t"
+        "selp.b32        %0, u0, %0, q;\n\t"
+        "selp.b32        %1, u1, %1, q;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+    return mk(r0, r1);
   }
   __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
 
+  // forward a: inputs weak; t = s y canonical -> single corrections
   __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
-    uint64_t t = mul(y, s);
-    uint64_t X = x;
-    x = add(X, t);
-    y = sub(X, t);
+    const uint64_t t = mul(y, s);
+    const uint64_t X = x;
+    x = add_c(X, t);
+    y = sub_c(X, t);
   }
+  // forward b: t = s x canonical; t + y single correction; t - y with weak y needs two
   __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
-    uint64_t t = mul(x, s);
-    uint64_t Y = y;
-    x = add(t, Y);
-    y = sub(t, Y);
+    const uint64_t t = mul(x, s);
+    const uint64_t Y = y;
+    x = add_c(Y, t);
+    y = sub_w(t, Y);
   }
+  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
   __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
-    uint64_t s = add(u, v);
-    uint64_t d = sub(u, v);
+    const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
+    const uint64_t d = sub_c(u, v);   // canonical
     u = mul(s, si);
     v = d;
   }
   __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
-    uint64_t s = add(u, v);
-    uint64_t d = sub(u, v);
-    u = canon(mul(s, si_k));
-    v = canon(mul(d, k));
+    const uint64_t s = add_c(u, v);
+    const uint64_t d = sub_c(u, v);
+    u = mul(s, si_k);
+    v = mul(d, k);
   }
   __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
   __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
-    return canon(mul(mul(a, b), k));
+    return mul(mul(a, b), k);
   }
 };
 
