@@ -1,16 +1,12 @@
-// api.cu — libfcirc C ABI (include/fcirc.h): validation, plan cache, workspace, dispatch.
-//
-// Pass schedule:
-//   n <= 2^MMAX  : one k_block launch with k = 0 (fused: one HBM read of a and b, one write of c)
-//   n >  2^MMAX  : per chunk of instances sized to stay L2-resident
-//                    k_cols<fwd>  top K = L - MMAX levels of a and b  -> a' (in c), b' (workspace)
-//                    k_block      the 2^K sub-products of size 2^MMAX  -> M (in c, in place)
-//                    k_cols<inv>  top K inverse levels, 1/n scaling     -> c (in place)
+// api.cu — libfcirc C ABI (include/fcirc.h): validation, plan cache, workspace, dispatch to the
+// per-field executors (matvec_u32.cu, matvec_gold.cu; pass schedule in matvec_impl.cuh) and the
+// applications (apps.cuh).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -19,9 +15,9 @@
 #include <vector>
 
 #include "../../include/fcirc.h"
-#include "fcirc_kernels.cuh"
-#include "plan.h"
 #include "apps.cuh"
+#include "plan.h"
+#include "runtime.h"
 
 namespace fcirc {
 
@@ -44,14 +40,14 @@ static cudaEvent_t prof_event() {
   cudaEventCreate(&e);
   return e;
 }
-static inline void prof_begin(int kind, cudaStream_t st) {
+void prof_begin(int kind, cudaStream_t st) {
   if (!g_prof_on) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   t_prof_kind = kind;
   t_prof_e0 = prof_event();
   cudaEventRecord(t_prof_e0, st);
 }
-static inline void prof_end(cudaStream_t st) {
+void prof_end(cudaStream_t st) {
   if (!g_prof_on || t_prof_kind < 0) return;
   std::lock_guard<std::mutex> lk(g_prof_mu);
   cudaEvent_t e1 = prof_event();
@@ -63,17 +59,12 @@ static inline void prof_end(cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 // device plans
 // ------------------------------------------------------------------------------------------
-struct DevPlan {
-  HostPlan hp;
-  void* twf = nullptr;  // TwU32[n] or uint64_t[n]
-  void* twi = nullptr;
-  TwU32 last_si32{}, last_k32{};
-  uint64_t last_si64 = 0, last_k64 = 0;
-  ~DevPlan() {
-    if (twf) cudaFree(twf);
-    if (twi) cudaFree(twi);
-  }
-};
+void count_launch() { ++g_launches; }
+
+DevPlan::~DevPlan() {
+  if (twf) cudaFree(twf);
+  if (twi) cudaFree(twi);
+}
 
 static std::mutex g_mu;
 static std::mutex g_host_mu;
@@ -133,7 +124,7 @@ struct Workspace {
 static std::map<std::tuple<int, void*, int>, Workspace> g_ws;
 
 // tag separates independent buffers of one call (0: matvec b', 1..: application scratch)
-static int get_workspace(int dev, void* stream, size_t bytes, void** out, int tag = 0) {
+int get_workspace(int dev, void* stream, size_t bytes, void** out, int tag) {
   std::lock_guard<std::mutex> lk(g_mu);
   Workspace& w = g_ws[std::make_tuple(dev, stream, tag)];
   if (w.bytes < bytes) {
@@ -150,86 +141,7 @@ static int get_workspace(int dev, void* stream, size_t bytes, void** out, int ta
   return FCIRC_OK;
 }
 
-// ------------------------------------------------------------------------------------------
-// kernel launch tables
-// ------------------------------------------------------------------------------------------
-template <class F> struct FTraits;
-template <> struct FTraits<FieldU32> { static constexpr int MMAX = 12; };
-template <> struct FTraits<FieldGold> { static constexpr int MMAX = 11; };
-constexpr int KMAX = 11;
-
-constexpr int rsel(int M) { return M < 4 ? (1 << M) : 16; }
-constexpr int ipcsel(int M) { return ((1 << M) / rsel(M)) >= 128 ? 1 : 128 / ((1 << M) / rsel(M)); }
-constexpr int wsel(int K) {
-  return (256 * rsel(K)) >> K < 8 ? 8 : ((256 * rsel(K)) >> K);
-}
-
-template <class F, int M>
-static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
-  constexpr int R = rsel(M), IPC = ipcsel(M);
-  constexpr int T = (1 << M) / R;
-  using E = typename F::T;
-  constexpr int PM = (1 << M) + ((1 << M) >> PadOf<E>::SH) + 1;
-  const size_t smem = (size_t)IPC * 2 * PM * sizeof(E);
-  auto kern = k_block<F, M, R, IPC>;
-  if (smem > 48 * 1024) {
-    static bool once = false;  // attribute set per kernel instantiation
-    if (!once) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return FCIRC_ECUDA;
-      once = true;
-    }
-  }
-  const int64_t grid = (args.units + IPC - 1) / IPC;
-  prof_begin(args.k == 0 ? 0 : 1, st);
-  kern<<<(unsigned)grid, T * IPC, smem, st>>>(fld, args);
-  prof_end(st);
-  ++g_launches;
-  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
-}
-
-template <class F, int K, bool INV>
-static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
-  constexpr int R = rsel(K), W = wsel(K);
-  constexpr int threads = W * ((1 << K) / R);
-  using E = typename F::T;
-  const size_t smem = (size_t)((1 << K) + ((1 << K) >> 4)) * W * sizeof(E);
-  auto kern = k_cols<F, K, R, W, INV>;
-  if (smem > 48 * 1024) {
-    static bool once = false;
-    if (!once) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return FCIRC_ECUDA;
-      once = true;
-    }
-  }
-  args.colblocks = args.m / W;
-  args.units = instances * args.colblocks;
-  dim3 grid((unsigned)args.units, INV ? 1 : 2);
-  prof_begin(INV ? 3 : 2, st);
-  kern<<<grid, threads, smem, st>>>(fld, args);
-  prof_end(st);
-  ++g_launches;
-  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
-}
-
-template <class F, int... Ms>
-static int dispatch_block(int M, const F& fld, const BlockArgs<F>& args, cudaStream_t st,
-                          std::integer_sequence<int, Ms...>) {
-  int rc = FCIRC_EINVAL;
-  ((M == Ms ? (rc = launch_block<F, Ms>(fld, args, st), 0) : 0), ...);
-  return rc;
-}
-
-template <class F, bool INV, int... Ks>
-static int dispatch_cols(int K, const F& fld, const ColArgs<F>& args, int64_t inst, cudaStream_t st,
-                         std::integer_sequence<int, Ks...>) {
-  int rc = FCIRC_EINVAL;
-  ((K == Ks + 1 ? (rc = launch_cols<F, Ks + 1, INV>(fld, args, inst, st), 0) : 0), ...);
-  return rc;
-}
-
-static size_t chunk_bytes() {
+size_t chunk_bytes() {
   static size_t v = [] {
     const char* e = getenv("FCIRC_CHUNK_BYTES");
     return e ? (size_t)strtoull(e, nullptr, 10) : (size_t)64 << 20;
@@ -237,46 +149,11 @@ static size_t chunk_bytes() {
   return v;
 }
 
-template <class F>
-static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
-                      int64_t batch, cudaStream_t st, int dev) {
-  using E = typename F::T;
-  using Tw = typename F::Tw;
-  constexpr int MMAX = FTraits<F>::MMAX;
-  const Tw* twf = (const Tw*)dp.twf;
-  const Tw* twi = (const Tw*)dp.twi;
-  Tw lsi, lk;
-  if constexpr (sizeof(E) == 4) { lsi = dp.last_si32; lk = dp.last_k32; }
-  else { lsi = dp.last_si64; lk = dp.last_k64; }
-  const int64_t n = (int64_t)1 << L;
-  if (L <= MMAX) {
-    BlockArgs<F> ba{(const E*)a, (const E*)b, (E*)c, batch, 0, twf, twi, lsi, lk};
-    return dispatch_block<F>(L, fld, ba, st, std::make_integer_sequence<int, MMAX + 1>{});
-  }
-  const int K = L - MMAX;
-  if (K > KMAX) return FCIRC_ESIZE;
-  const int64_t per_inst = 2 * n * (int64_t)sizeof(E);
-  int64_t C = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)chunk_bytes() / per_inst));
-  void* ws;
-  int rc = get_workspace(dev, (void*)st, (size_t)(C * n) * sizeof(E), &ws);
-  if (rc) return rc;
-  for (int64_t i0 = 0; i0 < batch; i0 += C) {
-    const int64_t cc = std::min<int64_t>(C, batch - i0);
-    const E* ai = (const E*)a + i0 * n;
-    const E* bi = (const E*)b + i0 * n;
-    E* ci = (E*)c + i0 * n;
-    E* bw = (E*)ws;
-    ColArgs<F> fa{ai, bi, ci, bw, n >> K, n, 0, 0, twf, twi, lsi, lk};
-    rc = dispatch_cols<F, false>(K, fld, fa, cc, st, std::make_integer_sequence<int, KMAX>{});
-    if (rc) return rc;
-    BlockArgs<F> ba{ci, bw, ci, cc << K, K, twf, twi, lsi, lk};
-    rc = launch_block<F, MMAX>(fld, ba, st);
-    if (rc) return rc;
-    ColArgs<F> ia{ci, nullptr, ci, nullptr, n >> K, n, 0, 0, twf, twi, lsi, lk};
-    rc = dispatch_cols<F, true>(K, fld, ia, cc, st, std::make_integer_sequence<int, KMAX>{});
-    if (rc) return rc;
-  }
-  return FCIRC_OK;
+int knob(const char* name, int dflt) {
+  char key[64];
+  snprintf(key, sizeof key, "FCIRC_%s", name);
+  const char* e = getenv(key);
+  return e ? atoi(e) : dflt;
 }
 
 static FieldU32 make_u32(uint64_t p) {
@@ -310,8 +187,7 @@ static int matvec_impl(uint64_t p, uint64_t f, const void* a, const void* b, voi
   const PrimeInfo* pi = prime_info(p);
   if (!pi) return FCIRC_EPRIME;
   const size_t es = pi->wide ? 8 : 4;
-  const int maxL = pi->wide ? FTraits<FieldGold>::MMAX + KMAX : FTraits<FieldU32>::MMAX + KMAX;
-  if (L > pi->two_adicity || L > maxL) return FCIRC_ESIZE;
+  if (L > pi->two_adicity || L > max_log_n(pi->wide)) return FCIRC_ESIZE;
   const size_t bytes = (size_t)n * (size_t)batch * es;
   if (overlaps(c, bytes, a, bytes) || overlaps(c, bytes, b, bytes)) return FCIRC_EINVAL;
   // Theorem 1 premises checked on the host before touching the device
@@ -323,9 +199,9 @@ static int matvec_impl(uint64_t p, uint64_t f, const void* a, const void* b, voi
   if (rc) return rc;
   if (pi->wide) {
     FieldGold fld;
-    return run_matvec(fld, *dp, a, b, c, L, batch, st, dev);
+    return run_matvec_gold(fld, *dp, a, b, c, L, batch, st, dev);
   }
-  return run_matvec(make_u32(p), *dp, a, b, c, L, batch, st, dev);
+  return run_matvec_u32(make_u32(p), *dp, a, b, c, L, batch, st, dev);
 }
 
 static int64_t next_pow2(int64_t x) {
@@ -518,8 +394,7 @@ int fcirc_polymul(uint64_t p, const void* a, int64_t na, const void* b, int64_t 
       overlaps(c, (size_t)(nc * batch) * es, b, (size_t)(nb * batch) * es))
     return FCIRC_EINVAL;
   const int64_t L = next_pow2(nc);
-  const int maxL = pi->wide ? FTraits<FieldGold>::MMAX + KMAX : FTraits<FieldU32>::MMAX + KMAX;
-  if (ilog2_exact(L) > pi->two_adicity || ilog2_exact(L) > maxL) return FCIRC_ESIZE;
+  if (ilog2_exact(L) > pi->two_adicity || ilog2_exact(L) > max_log_n(pi->wide)) return FCIRC_ESIZE;
   cudaStream_t st = (cudaStream_t)stream;
   if (pi->wide)
     return polymul_impl<uint64_t>(p, (const uint64_t*)a, na, (const uint64_t*)b, nb, (uint64_t*)c, batch, st, 1);

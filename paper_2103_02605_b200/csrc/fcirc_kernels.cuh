@@ -75,8 +75,8 @@ struct BlockArgs {
   typename F::Tw last_k;    // K = n^-1 (x R for FieldU32)
 };
 
-template <class F, int M, int R, int IPC>
-__global__ void __launch_bounds__((1 << M) / R * IPC)
+template <class F, int M, int R, int IPC, int MINB = 1>
+__global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
 k_block(F fld, BlockArgs<F> args) {
   using T = typename F::T;
   using Tw = typename F::Tw;
@@ -224,8 +224,8 @@ struct ColArgs {
   typename F::Tw last_k;
 };
 
-template <class F, int K, int R, int W, bool INV>
-__global__ void __launch_bounds__(W * ((1 << K) / R))
+template <class F, int K, int R, int W, bool INV, int MINB = 1>
+__global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols(F fld, ColArgs<F> args) {
   using T = typename F::T;
   using Tw = typename F::Tw;

@@ -1,0 +1,13 @@
+// matvec_gold.cu — the f-circulant product executor for Goldilocks p = 2^64 - 2^32 + 1 (FieldGold).
+#include "matvec_impl.cuh"
+
+namespace fcirc {
+
+int run_matvec_gold(const FieldGold& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
+                    int64_t batch, cudaStream_t st, int dev) {
+  return run_matvec(fld, dp, a, b, c, L, batch, st, dev);
+}
+
+int max_log_n(bool wide) { return (wide ? FTraits<FieldGold>::MMAX : FTraits<FieldU32>::MMAX) + KMAX; }
+
+}  // namespace fcirc

@@ -1,0 +1,174 @@
+// matvec_impl.cuh — launch tables and the pass schedule of the f-circulant product (SURVEY §8(a)
+// row H6), instantiated once per field by matvec_u32.cu / matvec_gold.cu.
+//
+//   n <= 2^MMAX  : one k_block launch with k = 0 (fused: one HBM read of a and b, one write of c)
+//   n >  2^MMAX  : per chunk of instances sized to stay L2-resident
+//                    k_cols<fwd>  top K = L - MMAX levels of a and b  -> a' (in c), b' (workspace)
+//                    k_block      the 2^K sub-products of size 2^MMAX  -> M (in c, in place)
+//                    k_cols<inv>  top K inverse levels, 1/n scaling     -> c (in place)
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <utility>
+
+#include "../../include/fcirc.h"
+#include "fcirc_kernels.cuh"
+#include "runtime.h"
+
+namespace fcirc {
+
+template <class F> struct FTraits;
+template <> struct FTraits<FieldU32> {
+  static constexpr int MMAX = 12;   // 2 x 2^12 x 4 B + pad = 33 KB smem per sub-problem
+  static constexpr const char* RB = "U32_RB";
+  static constexpr const char* RC = "U32_RC";
+};
+template <> struct FTraits<FieldGold> {
+  static constexpr int MMAX = 11;   // 2 x 2^11 x 8 B + pad = 35 KB smem per sub-problem
+  static constexpr const char* RB = "GOLD_RB";
+  static constexpr const char* RC = "GOLD_RC";
+};
+constexpr int KMAX = 11;
+
+// elements per thread (registers) for a transform of 2^M points; threads = 2^M / R
+template <int RR> constexpr int rsel(int M) { return M < 4 ? (1 << M) : RR; }
+template <int RR> constexpr int ipcsel(int M) {
+  return ((1 << M) / rsel<RR>(M)) >= 128 ? 1 : 128 / ((1 << M) / rsel<RR>(M));
+}
+// consecutive columns per k_cols CTA: >= 8 for 64-byte row segments, ~256 threads per CTA
+template <int RR> constexpr int wsel(int K) {
+  return (256 * rsel<RR>(K)) >> K < 8 ? 8 : ((256 * rsel<RR>(K)) >> K);
+}
+
+template <class F, int M, int RR>
+static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
+  constexpr int R = rsel<RR>(M), IPC = ipcsel<RR>(M);
+  constexpr int T = (1 << M) / R;
+  using E = typename F::T;
+  constexpr int PM = (1 << M) + ((1 << M) >> PadOf<E>::SH) + 1;
+  const size_t smem = (size_t)IPC * 2 * PM * sizeof(E);
+  // the R = 8 variants target 1024 resident threads per SM (register cap 64)
+  constexpr int MINB = (RR == 8 && T * IPC < 1024) ? 1024 / (T * IPC) : 1;
+  auto kern = k_block<F, M, R, IPC, MINB>;
+  if (smem > 48 * 1024) {
+    static bool once = false;  // attribute set per kernel instantiation
+    if (!once) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return FCIRC_ECUDA;
+      once = true;
+    }
+  }
+  const int64_t grid = (args.units + IPC - 1) / IPC;
+  prof_begin(args.k == 0 ? 0 : 1, st);
+  kern<<<(unsigned)grid, T * IPC, smem, st>>>(fld, args);
+  prof_end(st);
+  count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+template <class F, int K, bool INV, int RR>
+static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
+  constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
+  constexpr int threads = W * ((1 << K) / R);
+  using E = typename F::T;
+  const size_t smem = (size_t)((1 << K) + ((1 << K) >> 4)) * W * sizeof(E);
+  constexpr int MINB = (RR == 8 && threads < 1024) ? 1024 / threads : 1;
+  auto kern = k_cols<F, K, R, W, INV, MINB>;
+  if (smem > 48 * 1024) {
+    static bool once = false;
+    if (!once) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return FCIRC_ECUDA;
+      once = true;
+    }
+  }
+  args.colblocks = args.m / W;
+  args.units = instances * args.colblocks;
+  dim3 grid((unsigned)args.units, INV ? 1 : 2);
+  prof_begin(INV ? 3 : 2, st);
+  kern<<<grid, threads, smem, st>>>(fld, args);
+  prof_end(st);
+  count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+// Register-blocking variants: the two largest sub-problem sizes and the deep column transforms
+// are instantiated with R = 16 and R = 8 elements per thread (runtime knob FCIRC_<field>_RB /
+// _RC, default 16); everything else uses R = 16.
+template <class F, int M>
+static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
+  if constexpr (M >= FTraits<F>::MMAX - 1) {
+    static const int r = knob(FTraits<F>::RB, 16);
+    if (r == 8) return launch_block<F, M, 8>(fld, args, st);
+  }
+  return launch_block<F, M, 16>(fld, args, st);
+}
+
+template <class F, int K, bool INV>
+static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cudaStream_t st) {
+  if constexpr (K >= 8 && K <= 10) {  // K = 11 with R = 8 would need 2048 threads
+    static const int r = knob(FTraits<F>::RC, 16);
+    if (r == 8) return launch_cols<F, K, INV, 8>(fld, args, inst, st);
+  }
+  return launch_cols<F, K, INV, 16>(fld, args, inst, st);
+}
+
+template <class F, int... Ms>
+static int dispatch_block(int M, const F& fld, const BlockArgs<F>& args, cudaStream_t st,
+                          std::integer_sequence<int, Ms...>) {
+  int rc = FCIRC_EINVAL;
+  ((M == Ms ? (rc = launch_block_r<F, Ms>(fld, args, st), 0) : 0), ...);
+  return rc;
+}
+
+template <class F, bool INV, int... Ks>
+static int dispatch_cols(int K, const F& fld, const ColArgs<F>& args, int64_t inst, cudaStream_t st,
+                         std::integer_sequence<int, Ks...>) {
+  int rc = FCIRC_EINVAL;
+  ((K == Ks + 1 ? (rc = launch_cols_r<F, Ks + 1, INV>(fld, args, inst, st), 0) : 0), ...);
+  return rc;
+}
+
+template <class F>
+static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
+                      int64_t batch, cudaStream_t st, int dev) {
+  using E = typename F::T;
+  using Tw = typename F::Tw;
+  constexpr int MMAX = FTraits<F>::MMAX;
+  const Tw* twf = (const Tw*)dp.twf;
+  const Tw* twi = (const Tw*)dp.twi;
+  Tw lsi, lk;
+  if constexpr (sizeof(E) == 4) { lsi = dp.last_si32; lk = dp.last_k32; }
+  else { lsi = dp.last_si64; lk = dp.last_k64; }
+  const int64_t n = (int64_t)1 << L;
+  if (L <= MMAX) {
+    BlockArgs<F> ba{(const E*)a, (const E*)b, (E*)c, batch, 0, twf, twi, lsi, lk};
+    return dispatch_block<F>(L, fld, ba, st, std::make_integer_sequence<int, MMAX + 1>{});
+  }
+  const int K = L - MMAX;
+  if (K > KMAX) return FCIRC_ESIZE;
+  const int64_t per_inst = 2 * n * (int64_t)sizeof(E);
+  int64_t C = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)chunk_bytes() / per_inst));
+  void* ws;
+  int rc = get_workspace(dev, (void*)st, (size_t)(C * n) * sizeof(E), &ws);
+  if (rc) return rc;
+  for (int64_t i0 = 0; i0 < batch; i0 += C) {
+    const int64_t cc = std::min<int64_t>(C, batch - i0);
+    const E* ai = (const E*)a + i0 * n;
+    const E* bi = (const E*)b + i0 * n;
+    E* ci = (E*)c + i0 * n;
+    E* bw = (E*)ws;
+    ColArgs<F> fa{ai, bi, ci, bw, n >> K, n, 0, 0, twf, twi, lsi, lk};
+    rc = dispatch_cols<F, false>(K, fld, fa, cc, st, std::make_integer_sequence<int, KMAX>{});
+    if (rc) return rc;
+    BlockArgs<F> ba{ci, bw, ci, cc << K, K, twf, twi, lsi, lk};
+    rc = launch_block_r<F, MMAX>(fld, ba, st);
+    if (rc) return rc;
+    ColArgs<F> ia{ci, nullptr, ci, nullptr, n >> K, n, 0, 0, twf, twi, lsi, lk};
+    rc = dispatch_cols<F, true>(K, fld, ia, cc, st, std::make_integer_sequence<int, KMAX>{});
+    if (rc) return rc;
+  }
+  return FCIRC_OK;
+}
+
+}  // namespace fcirc

@@ -102,99 +102,97 @@ struct FieldGold {
   static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
   static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
 
-  // All helpers work on 32-bit halves with explicit PTX carry chains (add.cc / addc / sub.cc /
-  // subc), so that ptxas emits IADD3 / IADD3.X with carry predicates instead of 64-bit compares
-  // and selects (profiles/r01a_ncu_full_k_block.txt: the compare/select form saturated the ALU
-  // pipe at ~53 instructions per modmul).
+  // All helpers work on 32-bit halves with explicit PTX carry chains.  A wrap-around correction
+  // (+-EPS when a 64-bit add/sub carried/borrowed) is applied arithmetically, never by setp /
+  // selp / predication: after a subtract chain `subc.u32 m, 0, 0` yields m = -borrow (0 or
+  // 0xffffffff = EPS's low word) and the correction is one more subtract chain; after an add
+  // chain `addc.u32 m, 0, 0` yields the carry and `mad.lo.cc m * EPS` adds the correction.  (PTX
+  // carry flags are the hardware carry: after an add, `subc m, 0, 0` gives carry - 1, NOT -carry,
+  // so add and subtract chains are never mixed.)  ptxas maps the materialisations to IMAD.X /
+  // IMAD on the FMA pipe, which offloads the saturated ALU pipe
+  // (profiles/r01c_ncu_full_k_block.txt: the predicated form spent ~11 SEL/ISETP/PLOP3 per modmul).
   __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
   __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
   __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
 
-  // a + b mod p for a any 64-bit value and b < p (canonical): one wrap correction suffices,
-  // since a + b - 2^64 + EPS < a + p - p <= 2^64 - 1.  Result weakly reduced.
+  // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS;
+  // a + b - 2^64 + EPS <= (2^64-1) + (p-1) - 2^64 + EPS = 2^64 - 2: no second carry.  Weak result.
   __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
     uint32_t s0, s1;
-    asm("{\n\t.reg .u32 c;\n\t.reg .pred q;\n\t"
+    asm("{\n\t.reg .u32 m;\n\t"
         "add.cc.u32  %0, %2, %4;\n\t"
         "addc.cc.u32 %1, %3, %5;\n\t"
-        "addc.u32    c, 0, 0;\n\t"                 // carry out of 2^64
-        "setp.ne.u32 q, c, 0;\n\t"
-        "@q add.cc.u32  %0, %0, 0xffffffff;\n\t"   // + EPS
-        "@q addc.u32    %1, %1, 0;\n\t"
+        "addc.u32    m, 0, 0;\n\t"                 // m = carry (0/1)
+        "mad.lo.cc.u32 %0, m, 0xffffffff, %0;\n\t" // + EPS * carry
+        "addc.u32    %1, %1, 0;\n\t"
         "}"
         : "=&r"(s0), "=&r"(s1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
     return mk(s0, s1);
   }
-  // a - b mod p for a any 64-bit value and b < p: on a borrow, a - b + 2^64 - EPS >= 2^64 - p - EPS + 1 > 0,
-  // so one correction suffices.  Result canonical if a is.
+  // a - b mod p for a any 64-bit value and b < p: on a borrow subtract EPS; the wrapped value is
+  // a - b + 2^64 >= 2^64 - p + 1 > EPS, so no second borrow.  Canonical if a is canonical.
   __device__ __forceinline__ static uint64_t sub_c(uint64_t a, uint64_t b) {
     uint32_t d0, d1;
-    asm("{\n\t.reg .u32 bw;\n\t.reg .pred q;\n\t"
+    asm("{\n\t.reg .u32 m;\n\t"
         "sub.cc.u32  %0, %2, %4;\n\t"
         "subc.cc.u32 %1, %3, %5;\n\t"
-        "subc.u32    bw, 0, 0;\n\t"                // -borrow
-        "setp.ne.u32 q, bw, 0;\n\t"
-        "@q sub.cc.u32  %0, %0, 0xffffffff;\n\t"   // - EPS
-        "@q subc.u32    %1, %1, 0;\n\t"
+        "subc.u32    m, 0, 0;\n\t"        // m = -borrow
+        "sub.cc.u32  %0, %0, m;\n\t"      // - EPS
+        "subc.u32    %1, %1, 0;\n\t"
         "}"
         : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
     return mk(d0, d1);
   }
-  // a - b mod p for any 64-bit a, b (two borrow corrections); result weakly reduced
+  // a - b mod p for any 64-bit a, b: up to two borrow corrections (the second only if
+  // b > a + p - 2^64 + EPS, i.e. both were large); result a - b + {0, p, 2p}, weakly reduced.
   __device__ __forceinline__ static uint64_t sub_w(uint64_t a, uint64_t b) {
     uint32_t d0, d1;
-    asm("{\n\t.reg .u32 bw;\n\t.reg .pred q;\n\t"
+    asm("{\n\t.reg .u32 m;\n\t"
         "sub.cc.u32  %0, %2, %4;\n\t"
         "subc.cc.u32 %1, %3, %5;\n\t"
-        "subc.u32    bw, 0, 0;\n\t"
-        "setp.ne.u32 q, bw, 0;\n\t"
-        "@q sub.cc.u32  %0, %0, 0xffffffff;\n\t"
-        "@q subc.cc.u32 %1, %1, 0;\n\t"
-        "@q subc.u32    bw, 0, 0;\n\t"             // a second borrow only if b >= p + a
-        "setp.ne.u32 q, bw, 0;\n\t"
-        "@q sub.cc.u32  %0, %0, 0xffffffff;\n\t"
-        "@q subc.u32    %1, %1, 0;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.cc.u32 %1, %1, 0;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.u32    %1, %1, 0;\n\t"
         "}"
         : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
     return mk(d0, d1);
   }
-  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
-  //   t = t0 + t1 2^32 + t2 2^64 + t3 2^96,  2^64 == EPS, 2^96 == -1 (mod p):
-  //   s = (t1:t0) - t3            (borrow -> s -= EPS, cannot borrow again)
-  //   s = s + t2 * EPS            (carry k1)
-  //   u = s + EPS                 (carry k2: s >= p)
-  //   result = (k1 | k2) ? u : s  (k1 = 1 implies s + EPS < p; k2 = 1 means u = s - p)
-  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
-    // 64x64 -> 128: ptxas expands mul.lo.u64 / mul.hi.u64 into four IMAD.WIDE.U32 with
-    // carry-in/out predicates (7 SASS instructions, measured in tools/gold_bench.cu)
-    const uint64_t lo = a * b, hi = __umul64hi(a, b);
-    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
-  }
   // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
-  //   s = (t1:t0) - t3            (borrow -> s -= EPS, cannot borrow again)
-  //   s = s + t2 * EPS            (carry k1)
-  //   u = s + EPS                 (carry k2: s >= p)
-  //   result = (k1 | k2) ? u : s  (k1 = 1 implies s + EPS < p; k2 = 1 means u = s - p)
+  //   V = (t1:t0) + t2 EPS - t3 as a 3-word signed value c 2^64 + (r1:r0), c in {-1, 0, 1}
+  //       (V in (-2^32, 2^65 - 2^33]);
+  //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
+  //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
+  //   canonicalise: u = r + EPS carries iff r >= p; then r += EPS * carry (mod 2^64) = r - p.
   __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
     uint32_t r0, r1;
-    asm("{\n\t.reg .u32 bw, k, u0, u1;\n\t.reg .pred q;\n\t"
-        "sub.cc.u32      %0, %2, %5;\n\t"
-        "subc.cc.u32     %1, %3, 0;\n\t"
-        "subc.u32        bw, 0, 0;\n\t"
-        "sub.cc.u32      %0, %0, bw;\n\t"
-        "subc.u32        %1, %1, 0;\n\t"
-        "mad.lo.cc.u32   %0, %4, 0xffffffff, %0;\n\t"
-        "madc.hi.cc.u32  %1, %4, 0xffffffff, %1;\n\t"
-        "addc.u32        k, 0, 0;\n\t"
-        "add.cc.u32      u0, %0, 0xffffffff;\n\t"
-        "addc.cc.u32     u1, %1, 0;\n\t"
-        "addc.u32        k, k, 0;\n\t"
-        "setp.ne.u32     q, k, 0;\n\t"
-        "selp.b32        %0, u0, %0, q;\n\t"
-        "selp.b32        %1, u1, %1, q;\n\t"
+    asm("{\n\t.reg .u32 c, m, h;\n\t"
+        "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
+        "madc.hi.cc.u32  %1, %4, 0xffffffff, %3;\n\t"
+        "addc.u32        c, 0, 0;\n\t"
+        "sub.cc.u32      %0, %0, %5;\n\t"
+        "subc.cc.u32     %1, %1, 0;\n\t"
+        "subc.u32        c, c, 0;\n\t"
+        "neg.s32         m, c;\n\t"
+        "shr.s32         h, c, 31;\n\t"
+        "add.cc.u32      %0, %0, m;\n\t"
+        "addc.u32        %1, %1, h;\n\t"
+        "add.cc.u32      m, %0, 0xffffffff;\n\t"   // carry out iff r >= p
+        "addc.cc.u32     h, %1, 0;\n\t"
+        "addc.u32        m, 0, 0;\n\t"
+        "mad.lo.cc.u32   %0, m, 0xffffffff, %0;\n\t"  // r + EPS * carry (mod 2^64) = r - p
+        "addc.u32        %1, %1, 0;\n\t"
         "}"
         : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
     return mk(r0, r1);
+  }
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+    // ptxas expands mul.lo.u64 / mul.hi.u64 into IMAD.WIDE.U32 chains with carry predicates
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
   }
   __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
 

@@ -1,0 +1,49 @@
+// runtime.h — internal (non-ABI) interface between the C-ABI layer (api.cu) and the per-field
+// executors of the f-circulant product (matvec_u32.cu, matvec_gold.cu).  Splitting the fields
+// into their own translation units lets the build compile them in parallel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "modarith.cuh"
+#include "plan.h"
+
+namespace fcirc {
+
+// A device-resident plan: the host tables of plan.h uploaded in the element layout of the field.
+struct DevPlan {
+  HostPlan hp;
+  void* twf = nullptr;  // TwU32[n] or uint64_t[n]: s_{d,e} at heap index 2^d + e
+  void* twi = nullptr;  // s_{d,e}^-1
+  TwU32 last_si32{}, last_k32{};
+  uint64_t last_si64 = 0, last_k64 = 0;
+  ~DevPlan();
+};
+
+// launch bookkeeping (api.cu): optional per-launch CUDA-event timing and the launch counter
+void prof_begin(int kind, cudaStream_t st);
+void prof_end(cudaStream_t st);
+void count_launch();
+
+// grow-only device scratch per (device, stream, tag) (api.cu)
+int get_workspace(int dev, void* stream, size_t bytes, void** out, int tag = 0);
+
+// integer tuning knob read once from the environment (FCIRC_<name>), else `dflt`
+int knob(const char* name, int dflt);
+
+// bytes of a' + b' intermediates per chunk of the multi-pass schedule (FCIRC_CHUNK_BYTES)
+size_t chunk_bytes();
+
+// Per-field executors: all launches of one batched product on `st`.
+// a, b, c: [batch][2^L] device arrays of the field's element type; c may not alias a or b.
+int run_matvec_u32(const FieldU32& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
+                   int64_t batch, cudaStream_t st, int dev);
+int run_matvec_gold(const FieldGold& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
+                    int64_t batch, cudaStream_t st, int dev);
+
+// largest supported log2 n of the executors (multi-pass: MMAX + KMAX)
+int max_log_n(bool wide);
+
+}  // namespace fcirc

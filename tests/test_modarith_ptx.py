@@ -1,0 +1,76 @@
+"""Host-side check of the Goldilocks inline-PTX carry chains in csrc/modarith.cuh.
+
+The chains are executed by tools/ptx_carry_sim.py under the hardware carry model ptxas uses (see
+its docstring) on edge and random operands and compared with Python integers.  This pins the
+contracts the kernels rely on: add_c(weak, canonical) and sub_c(weak, canonical)
+need one correction, sub_w(weak, weak) two, and the 128 -> 64 reduction returns the canonical
+residue.  A GPU re-check of the same helpers runs in tools/gold_bench.cu.
+"""
+import os
+import random
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import ptx_carry_sim as sim  # noqa: E402
+
+P = (1 << 64) - (1 << 32) + 1
+M64 = (1 << 64) - 1
+SRC = open(os.path.join(ROOT, "paper_2103_02605_b200", "csrc", "modarith.cuh")).read()
+SRC = SRC[SRC.index("struct FieldGold {"):]
+
+EDGE = [0, 1, 2, P - 2, P - 1, P, P + 1, M64, M64 - 1, 0xFFFFFFFF, 1 << 32, (1 << 32) + 1,
+        0x8000000000000000, 0xFFFFFFFF00000000, 0xFFFFFFFEFFFFFFFF, 0x00000000FFFFFFFE]
+
+
+def _pairs(rng, n=3000, a_max=M64, b_max=M64):
+    for a in EDGE:
+        for b in EDGE:
+            if a <= a_max and b <= b_max:
+                yield a, b
+    for _ in range(n):
+        yield rng.randint(0, a_max), rng.randint(0, b_max)
+        yield rng.randint(max(0, a_max - (1 << 34)), a_max), rng.randint(max(0, b_max - (1 << 34)), b_max)
+
+
+def test_add_c_weak_plus_canonical():
+    f = sim.helper(SRC, "add_c")
+    for a, b in _pairs(random.Random(1), b_max=P - 1):
+        r = f(a, b)
+        assert r % P == (a + b) % P, (a, b, r)
+
+
+def test_sub_c_weak_minus_canonical():
+    f = sim.helper(SRC, "sub_c")
+    for a, b in _pairs(random.Random(2), b_max=P - 1):
+        r = f(a, b)
+        assert r % P == (a - b) % P, (a, b, r)
+        if a < P:
+            assert r < P, "canonical minus canonical must stay canonical"
+
+
+def test_sub_w_weak_minus_weak():
+    f = sim.helper(SRC, "sub_w")
+    for a, b in _pairs(random.Random(3)):
+        r = f(a, b)
+        assert r % P == (a - b) % P, (a, b, r)
+
+
+@pytest.mark.parametrize("seed", [4, 5])
+def test_reduce4_canonical(seed):
+    f = sim.helper(SRC, "reduce4")
+    rng = random.Random(seed)
+    words = [0, 1, 0xFFFFFFFF, 0xFFFFFFFE, 0x80000000]
+    cases = [(a, b, c, d) for a in words for b in words for c in words for d in words]
+    cases += [tuple(rng.getrandbits(32) for _ in range(4)) for _ in range(4000)]
+    # full products of extreme operands
+    for x in EDGE:
+        for y in EDGE:
+            t = x * y
+            cases.append(tuple((t >> (32 * i)) & 0xFFFFFFFF for i in range(4)))
+    for t0, t1, t2, t3 in cases:
+        v = t0 | (t1 << 32) | (t2 << 64) | (t3 << 96)
+        r = f(t0, t1, t2, t3)
+        assert r == v % P, (hex(v), hex(r))

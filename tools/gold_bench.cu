@@ -7,6 +7,148 @@
 #include "../paper_2103_02605_b200/csrc/modarith.cuh"
 
 using namespace fcirc;
+
+namespace fcirc {
+// ------------------------------------------------------------------------------------------
+// Goldilocks p = 2^64 - 2^32 + 1
+// ------------------------------------------------------------------------------------------
+struct FieldGoldSel {  // r01b variant (predicated corrections), kept for comparison
+  using T = uint64_t;
+  using Tw = uint64_t;
+  static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
+  static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
+
+  // All helpers work on 32-bit halves with explicit PTX carry chains (add.cc / addc / sub.cc /
+  // subc), so that ptxas emits IADD3 / IADD3.X with carry predicates instead of 64-bit compares
+  // and selects (profiles/r01a_ncu_full_k_block.txt: the compare/select form saturated the ALU
+  // pipe at ~53 instructions per modmul).
+  __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+  __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+  // a + b mod p for a any 64-bit value and b < p (canonical): one wrap correction suffices,
+  // since a + b - 2^64 + EPS < a + p - p <= 2^64 - 1.  Result weakly reduced.
+  __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
+    uint32_t s0, s1;
+    asm("{\n\t.reg .u32 c;\n\t.reg .pred q;\n\t"
+        "add.cc.u32  %0, %2, %4;\n\t"
+        "addc.cc.u32 %1, %3, %5;\n\t"
+        "addc.u32    c, 0, 0;\n\t"                 // carry out of 2^64
+        "setp.ne.u32 q, c, 0;\n\t"
+        "@q add.cc.u32  %0, %0, 0xffffffff;\n\t"   // + EPS
+        "@q addc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(s0), "=&r"(s1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(s0, s1);
+  }
+  // a - b mod p for a any 64-bit value and b < p: on a borrow, a - b + 2^64 - EPS >= 2^64 - p - EPS + 1 > 0,
+  // so one correction suffices.  Result canonical if a is.
+  __device__ __forceinline__ static uint64_t sub_c(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 bw;\n\t.reg .pred q;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    bw, 0, 0;\n\t"                // -borrow
+        "setp.ne.u32 q, bw, 0;\n\t"
+        "@q sub.cc.u32  %0, %0, 0xffffffff;\n\t"   // - EPS
+        "@q subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // a - b mod p for any 64-bit a, b (two borrow corrections); result weakly reduced
+  __device__ __forceinline__ static uint64_t sub_w(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 bw;\n\t.reg .pred q;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    bw, 0, 0;\n\t"
+        "setp.ne.u32 q, bw, 0;\n\t"
+        "@q sub.cc.u32  %0, %0, 0xffffffff;\n\t"
+        "@q subc.cc.u32 %1, %1, 0;\n\t"
+        "@q subc.u32    bw, 0, 0;\n\t"             // a second borrow only if b >= p + a
+        "setp.ne.u32 q, bw, 0;\n\t"
+        "@q sub.cc.u32  %0, %0, 0xffffffff;\n\t"
+        "@q subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  //   t = t0 + t1 2^32 + t2 2^64 + t3 2^96,  2^64 == EPS, 2^96 == -1 (mod p):
+  //   s = (t1:t0) - t3            (borrow -> s -= EPS, cannot borrow again)
+  //   s = s + t2 * EPS            (carry k1)
+  //   u = s + EPS                 (carry k2: s >= p)
+  //   result = (k1 | k2) ? u : s  (k1 = 1 implies s + EPS < p; k2 = 1 means u = s - p)
+  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+    // 64x64 -> 128: ptxas expands mul.lo.u64 / mul.hi.u64 into four IMAD.WIDE.U32 with
+    // carry-in/out predicates (7 SASS instructions, measured in tools/gold_bench.cu)
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
+  //   s = (t1:t0) - t3            (borrow -> s -= EPS, cannot borrow again)
+  //   s = s + t2 * EPS            (carry k1)
+  //   u = s + EPS                 (carry k2: s >= p)
+  //   result = (k1 | k2) ? u : s  (k1 = 1 implies s + EPS < p; k2 = 1 means u = s - p)
+  __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 bw, k, u0, u1;\n\t.reg .pred q;\n\t"
+        "sub.cc.u32      %0, %2, %5;\n\t"
+        "subc.cc.u32     %1, %3, 0;\n\t"
+        "subc.u32        bw, 0, 0;\n\t"
+        "sub.cc.u32      %0, %0, bw;\n\t"
+        "subc.u32        %1, %1, 0;\n\t"
+        "mad.lo.cc.u32   %0, %4, 0xffffffff, %0;\n\t"
+        "madc.hi.cc.u32  %1, %4, 0xffffffff, %1;\n\t"
+        "addc.u32        k, 0, 0;\n\t"
+        "add.cc.u32      u0, %0, 0xffffffff;\n\t"
+        "addc.cc.u32     u1, %1, 0;\n\t"
+        "addc.u32        k, k, 0;\n\t"
+        "setp.ne.u32     q, k, 0;\n\t"
+        "selp.b32        %0, u0, %0, q;\n\t"
+        "selp.b32        %1, u1, %1, q;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+    return mk(r0, r1);
+  }
+  __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
+
+  // forward a: inputs weak; t = s y canonical -> single corrections
+  __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(y, s);
+    const uint64_t X = x;
+    x = add_c(X, t);
+    y = sub_c(X, t);
+  }
+  // forward b: t = s x canonical; t + y single correction; t - y with weak y needs two
+  __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(x, s);
+    const uint64_t Y = y;
+    x = add_c(Y, t);
+    y = sub_w(t, Y);
+  }
+  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
+  __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
+    const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
+    const uint64_t d = sub_c(u, v);   // canonical
+    u = mul(s, si);
+    v = d;
+  }
+  __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
+    const uint64_t s = add_c(u, v);
+    const uint64_t d = sub_c(u, v);
+    u = mul(s, si_k);
+    v = mul(d, k);
+  }
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
+    return mul(mul(a, b), k);
+  }
+};
+
+}  // namespace fcirc
+
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { fprintf(stderr, "CUDA %s line %d\n", cudaGetErrorString(e_), __LINE__); return 1; } } while (0)
 
 constexpr uint64_t P = 0xFFFFFFFF00000001ull;
@@ -22,9 +164,9 @@ __device__ __forceinline__ uint64_t ref_sub(uint64_t a, uint64_t b) {
 
 constexpr int CH = 8, IT = 1024;
 
-template <int KIND>
+template <class FG, int KIND>
 __global__ void __launch_bounds__(256) k_tp(uint64_t* out, uint64_t seed) {
-  FieldGold F;
+  FG F;
   uint64_t x[CH], y[CH];
   for (int c = 0; c < CH; ++c) { x[c] = seed * (threadIdx.x + 1) + c * 0x9E3779B97F4A7C15ull; y[c] = x[c] ^ 0xDEADBEEFCAFEF00Dull; }
   const uint64_t w = 0x1234567890ABCDEFull ^ seed;
@@ -43,8 +185,9 @@ __global__ void __launch_bounds__(256) k_tp(uint64_t* out, uint64_t seed) {
 }
 
 // correctness: random and edge operands vs reference
+template <class FG>
 __global__ void k_check(unsigned long long* bad, uint64_t seed) {
-  FieldGold F;
+  FG F;
   const uint64_t edge[] = {0, 1, 2, P - 1, P, P + 1, 0xFFFFFFFFFFFFFFFFull, 0xFFFFFFFF00000000ull,
                            0x00000000FFFFFFFFull, 0x8000000000000000ull, 0xFFFFFFFEFFFFFFFFull, P - 2};
   uint64_t s = seed ^ (threadIdx.x + blockIdx.x * 977ull);
@@ -76,15 +219,15 @@ __global__ void k_check(unsigned long long* bad, uint64_t seed) {
   }
 }
 
-template <int KIND>
+template <class FG, int KIND>
 static int tp(const char* name, int nsm) {
   uint64_t* d; CK(cudaMalloc(&d, 64));
   cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
   const int blocks = nsm * 4, thr = 256;
-  k_tp<KIND><<<blocks, thr>>>(d, 1); CK(cudaDeviceSynchronize());
+  k_tp<FG, KIND><<<blocks, thr>>>(d, 1); CK(cudaDeviceSynchronize());
   float best = 1e9f;
   for (int r = 0; r < 5; ++r) {
-    CK(cudaEventRecord(e0)); k_tp<KIND><<<blocks, thr>>>(d, r + 2); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventRecord(e0)); k_tp<FG, KIND><<<blocks, thr>>>(d, r + 2); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
     float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); if (ms < best) best = ms;
   }
   double ops = (double)blocks * thr * CH * IT;
@@ -94,15 +237,23 @@ static int tp(const char* name, int nsm) {
   return 0;
 }
 
+template <class FG>
+static int run(const char* tag, int nsm) {
+  unsigned long long* bad; CK(cudaMalloc(&bad, 5 * 8)); CK(cudaMemset(bad, 0, 5 * 8));
+  k_check<FG><<<148, 256>>>(bad, 12345); CK(cudaDeviceSynchronize());
+  unsigned long long h[5]; CK(cudaMemcpy(h, bad, 40, cudaMemcpyDeviceToHost));
+  printf("{\"field\": \"%s\", \"check_bad\": [%llu, %llu, %llu, %llu, %llu]}\n", tag, h[0], h[1], h[2], h[3], h[4]);
+  printf("# %s\n", tag);
+  tp<FG, 0>("fwd_a butterfly", nsm);
+  tp<FG, 1>("fwd_b butterfly", nsm);
+  tp<FG, 2>("inv butterfly", nsm);
+  tp<FG, 3>("mul chain", nsm);
+  return (h[0] | h[1] | h[2] | h[3] | h[4]) ? 2 : 0;
+}
+
 int main() {
   int nsm; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
-  unsigned long long* bad; CK(cudaMalloc(&bad, 5 * 8)); CK(cudaMemset(bad, 0, 5 * 8));
-  k_check<<<148, 256>>>(bad, 12345); CK(cudaDeviceSynchronize());
-  unsigned long long h[5]; CK(cudaMemcpy(h, bad, 40, cudaMemcpyDeviceToHost));
-  printf("{\"check_bad\": [%llu, %llu, %llu, %llu, %llu]}\n", h[0], h[1], h[2], h[3], h[4]);
-  tp<0>("fwd_a butterfly", nsm);
-  tp<1>("fwd_b butterfly", nsm);
-  tp<2>("inv butterfly", nsm);
-  tp<3>("mul chain", nsm);
-  return (h[0] | h[1] | h[2] | h[3] | h[4]) ? 2 : 0;
+  int rc = run<FieldGoldSel>("r01b predicated corrections (FieldGoldSel)", nsm);
+  rc |= run<FieldGold>("mask corrections (FieldGold, current)", nsm);
+  return rc;
 }

@@ -1,0 +1,107 @@
+#!/usr/bin/env python
+"""Interpreter for the inline-PTX carry chains of csrc/modarith.cuh (dev/test tool, CPU only).
+
+Extracts each `asm(...)` block of a named FieldGold helper and executes it on 32-bit words with
+the carry model ptxas implements (checked in the SASS: after an add chain `subc.u32 m, 0, 0`
+becomes `IMAD.X m, RZ, RZ, -1, P` = carry - 1):
+
+    CF is the hardware carry.  add.cc:  d = a + b,        CF = carry out
+                                addc:    d = a + b + CF
+                                sub.cc:  d = a + ~b + 1,   CF = carry out (= NOT borrow)
+                                subc:    d = a + ~b + CF
+                                mad.lo.cc / madc.hi.cc: lo/hi 32 bits of a*b, plus c (+ CF)
+
+so a helper can be checked exhaustively on edge values and randomly against Python integers
+without a GPU.  Used by tests/test_modarith_ptx.py.
+"""
+from __future__ import annotations
+
+import re
+
+M32 = 0xFFFFFFFF
+
+
+def extract(src: str, fn: str):
+    """(asm text, operand constraint list) of the first asm block inside function `fn`."""
+    i = src.index(f" {fn}(")
+    j = src.index("asm(", i)
+    k = src.index(");", j)
+    block = src[j + 4:k]
+    parts = block.split(":")
+    text = "".join(re.findall(r'"((?:[^"\\]|\\.)*)"', parts[0]))
+    text = text.replace("\\n", "\n").replace("\\t", " ")
+    outs = re.findall(r'"=&?r"', parts[1]) if len(parts) > 1 else []
+    ins = re.findall(r'"r"', parts[2]) if len(parts) > 2 else []
+    return text, len(outs), len(ins)
+
+
+def run(text: str, nout: int, inputs):
+    regs = {}
+    for i, v in enumerate(inputs):
+        regs[f"%{nout + i}"] = v & M32
+    for i in range(nout):
+        regs[f"%{i}"] = 0
+    cf = 0
+
+    def val(tok):
+        tok = tok.strip()
+        if tok in regs:
+            return regs[tok]
+        return int(tok, 0) & M32
+
+    for line in text.split("\n"):
+        line = line.strip().rstrip(";")
+        if not line or line in "{}" or line.startswith(".reg") or line.startswith("//"):
+            continue
+        line = line.split("//")[0].strip().rstrip(";")
+        op, rest = line.split(None, 1)
+        args = [a.strip() for a in rest.split(",")]
+        d = args[0]
+        if op in ("add.cc.u32", "addc.cc.u32", "addc.u32", "add.u32"):
+            cin = cf if op.startswith("addc") else 0
+            r = val(args[1]) + val(args[2]) + cin
+            if ".cc" in op:
+                cf = r >> 32
+        elif op in ("sub.cc.u32", "subc.cc.u32", "subc.u32", "sub.u32"):
+            cin = cf if op.startswith("subc") else 1
+            r = val(args[1]) + ((~val(args[2])) & M32) + cin
+            if ".cc" in op:
+                cf = r >> 32
+        elif op in ("mad.lo.cc.u32", "madc.lo.cc.u32", "mad.lo.u32", "madc.lo.u32"):
+            cin = cf if op.startswith("madc") else 0
+            r = ((val(args[1]) * val(args[2])) & M32) + val(args[3]) + cin
+            if ".cc" in op:
+                cf = r >> 32
+        elif op in ("mad.hi.cc.u32", "madc.hi.cc.u32", "mad.hi.u32", "madc.hi.u32"):
+            cin = cf if op.startswith("madc") else 0
+            r = ((val(args[1]) * val(args[2])) >> 32) + val(args[3]) + cin
+            if ".cc" in op:
+                cf = r >> 32
+        elif op == "neg.s32":
+            r = -val(args[1])
+        elif op == "shr.s32":
+            x = val(args[1])
+            if x >> 31:
+                x -= 1 << 32
+            r = x >> int(args[2])
+        elif op == "mov.u32":
+            r = val(args[1])
+        else:
+            raise ValueError(f"unsupported PTX op {op!r}")
+        regs[d] = r & M32
+    return [regs[f"%{i}"] for i in range(nout)]
+
+
+def helper(src: str, fn: str):
+    """Python callable on 64-bit values for FieldGold.<fn> (add_c, sub_c, sub_w) or reduce4."""
+    text, nout, nin = extract(src, fn)
+    if fn == "reduce4":
+        def f(t0, t1, t2, t3):
+            r0, r1 = run(text, nout, [t0, t1, t2, t3])
+            return r0 | (r1 << 32)
+        return f
+
+    def g(a, b):
+        r0, r1 = run(text, nout, [a & M32, a >> 32, b & M32, b >> 32])
+        return r0 | (r1 << 32)
+    return g
