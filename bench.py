@@ -56,7 +56,7 @@ WORKLOADS = {
     **{f"C4_n{L}": dict(cfg=f"C4_n{L}", desc=f"C4 @ n=2^{L}: Goldilocks f-circulant matvec, batch 2^{26 - L}")
        for L in range(12, 23) if L != 20},
 }
-MMAX = {"u64": 11, "u32": 12}
+MMAX = {"u64": 12, "u32": 13}  # fcirc_max_fused_log2 (matvec_impl.cuh FTraits::MMAX)
 
 
 def measured_peaks():
@@ -140,6 +140,30 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ helpers
+
+def rank_config(cfg: dict, rank: int) -> dict:
+    """Per-rank workload: every rank draws its own independent instances of the
+    same configuration (weak scaling, no data-path collective)."""
+    out = dict(cfg)
+    out["seed"] = out["seed"] + 7919 * rank
+    return out
+
+
+def max_over_ranks(x: float, world: int, device="cuda") -> float:
+    """Max of a per-rank scalar over all ranks (the timing rule: slowest rank defines the step)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_gelems(world: int, batch: int, n: int, steps: int, ms_max: float) -> float:
+    """Whole-job throughput: elements of all ranks / the slowest rank's time."""
+    return world * batch * n * steps / (ms_max * 1e-3) / 1e9
+
 
 def algorithmic_modmuls(kind: str, n: int, batch: int, width: str) -> float:
     """Algorithmic modmuls per step attributed to one kernel kind:
@@ -240,8 +264,7 @@ def run_fcirc(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = WORKLOADS[args.config]
     cfg = {k: v for k, v in synth.CONFIGS[w["cfg"]].items() if k != "kind"}
-    cfg["seed"] = cfg["seed"] + 7919 * rank       # each rank its own instances
-    inp = synth.matvec_inputs(**cfg)
+    inp = synth.matvec_inputs(**rank_config(cfg, rank))
     p, f, n, batch = inp["p"], inp["f"], inp["n"], inp["batch"]
     width = cfg_dtype(p)
     a = torch.from_numpy(inp["a"]).cuda()
@@ -278,13 +301,9 @@ def run_fcirc(args):
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms, world)
     ms_step = ms_max / args.steps
-    elems = world * batch * n * args.steps
-    value = elems / (ms_max * 1e-3) / 1e9
+    value = whole_job_gelems(world, batch, n, args.steps, ms_max)
 
     # ---- roofline of the dominant kernel
     dom = max((k for k in prof if prof[k][0] > 0), key=lambda k: prof[k][1])
@@ -326,11 +345,7 @@ def run_fcirc(args):
         t0 = time.perf_counter()
         for _ in range(e_steps):
             fc.matvec_host(ha, hb, f, p, out=hc)
-        dt = time.perf_counter() - t0
-        td = torch.tensor([dt], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(td, op=dist.ReduceOp.MAX)
-        dt = float(td.item())
+        dt = max_over_ranks(time.perf_counter() - t0, world)
         esz = 8 if width == "u64" else 4
         e2e = {"value": world * batch * n * e_steps / dt / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": 2 * batch * n * esz, "d2h_bytes_per_step": batch * n * esz,
@@ -369,7 +384,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=3.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -144,7 +144,7 @@ int get_workspace(int dev, void* stream, size_t bytes, void** out, int tag) {
 size_t chunk_bytes() {
   static size_t v = [] {
     const char* e = getenv("FCIRC_CHUNK_BYTES");
-    return e ? (size_t)strtoull(e, nullptr, 10) : (size_t)64 << 20;
+    return e ? (size_t)strtoull(e, nullptr, 10) : (size_t)1 << 30;  // profiles/r01c_sweep.txt
   }();
   return v;
 }

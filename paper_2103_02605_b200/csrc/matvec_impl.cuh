@@ -19,12 +19,12 @@ namespace fcirc {
 
 template <class F> struct FTraits;
 template <> struct FTraits<FieldU32> {
-  static constexpr int MMAX = 12;   // 2 x 2^12 x 4 B + pad = 33 KB smem per sub-problem
+  static constexpr int MMAX = 13;   // 2 x 2^13 x 4 B + pad = 66 KB smem per sub-problem
   static constexpr const char* RB = "U32_RB";
   static constexpr const char* RC = "U32_RC";
 };
 template <> struct FTraits<FieldGold> {
-  static constexpr int MMAX = 11;   // 2 x 2^11 x 8 B + pad = 35 KB smem per sub-problem
+  static constexpr int MMAX = 12;   // 2 x 2^12 x 8 B + pad = 70 KB smem per sub-problem
   static constexpr const char* RB = "GOLD_RB";
   static constexpr const char* RC = "GOLD_RC";
 };
@@ -47,8 +47,9 @@ static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st)
   using E = typename F::T;
   constexpr int PM = (1 << M) + ((1 << M) >> PadOf<E>::SH) + 1;
   const size_t smem = (size_t)IPC * 2 * PM * sizeof(E);
-  // the R = 8 variants target 1024 resident threads per SM (register cap 64)
-  constexpr int MINB = (RR == 8 && T * IPC < 1024) ? 1024 / (T * IPC) : 1;
+  // occupancy target: 1024 resident threads per SM for R <= 8 (register cap 64), 512 for R = 16
+  // (cap 128: without a floor ptxas spends ~190 registers and halves the resident warps)
+  constexpr int MINB = (T * IPC < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / (T * IPC) : 1;
   auto kern = k_block<F, M, R, IPC, MINB>;
   if (smem > 48 * 1024) {
     static bool once = false;  // attribute set per kernel instantiation
@@ -72,7 +73,7 @@ static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStr
   constexpr int threads = W * ((1 << K) / R);
   using E = typename F::T;
   const size_t smem = (size_t)((1 << K) + ((1 << K) >> 4)) * W * sizeof(E);
-  constexpr int MINB = (RR == 8 && threads < 1024) ? 1024 / threads : 1;
+  constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
   auto kern = k_cols<F, K, R, W, INV, MINB>;
   if (smem > 48 * 1024) {
     static bool once = false;
@@ -92,23 +93,33 @@ static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStr
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
 
-// Register-blocking variants: the two largest sub-problem sizes and the deep column transforms
-// are instantiated with R = 16 and R = 8 elements per thread (runtime knob FCIRC_<field>_RB /
-// _RC, default 16); everything else uses R = 16.
+// Register-blocking variants: the two largest sub-problem sizes and the deep column
+// transforms are instantiated with R = 16, 8 and 4 elements per thread, selected by the runtime
+// knobs FCIRC_<field>_RB / _RC (defaults from the measured sweep, profiles/r01c_sweep.txt).
+// Smaller R = more threads per sub-problem and fewer registers per thread: more resident warps to
+// hide the latency of the carry chains, at the price of more shared-memory exchange phases.
+template <class F> struct RDefault;
+template <> struct RDefault<FieldU32> { static constexpr int RB = 8, RC = 16; };
+template <> struct RDefault<FieldGold> { static constexpr int RB = 8, RC = 8; };
+
 template <class F, int M>
 static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
   if constexpr (M >= FTraits<F>::MMAX - 1) {
-    static const int r = knob(FTraits<F>::RB, 16);
+    static const int r = knob(FTraits<F>::RB, RDefault<F>::RB);
     if (r == 8) return launch_block<F, M, 8>(fld, args, st);
+    if constexpr ((1 << M) / 4 <= 1024)  // one sub-problem per CTA: at most 1024 threads
+      if (r == 4) return launch_block<F, M, 4>(fld, args, st);
   }
   return launch_block<F, M, 16>(fld, args, st);
 }
 
 template <class F, int K, bool INV>
 static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cudaStream_t st) {
-  if constexpr (K >= 8 && K <= 10) {  // K = 11 with R = 8 would need 2048 threads
-    static const int r = knob(FTraits<F>::RC, 16);
+  if constexpr (K >= 6 && K <= 10) {  // K = 11 with R = 8 would need 2048 threads
+    static const int r = knob(FTraits<F>::RC, RDefault<F>::RC);
     if (r == 8) return launch_cols<F, K, INV, 8>(fld, args, inst, st);
+    if constexpr (K <= 9)
+      if (r == 4) return launch_cols<F, K, INV, 4>(fld, args, inst, st);
   }
   return launch_cols<F, K, INV, 16>(fld, args, inst, st);
 }

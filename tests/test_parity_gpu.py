@@ -117,13 +117,14 @@ def test_matvec_extreme_values():
 
 @pytest.mark.parametrize("p", PRIMES)
 def test_matvec_multipass_sampled(p):
-    """n = 2^13 .. 2^22 (2^23 for 998244353): three-pass schedule, sampled entries + checksum."""
-    top = 23 if p == P998 else 22
+    """n = 2^13 .. the maximum (2^23, or 2^24 for the primes with 2-adicity > 23): three-pass
+    schedule, sampled entries + checksum."""
+    top = {P998: 23, P469: 24, P167: 24, GOLDILOCKS: 23}[p]
     for L in range(13, top + 1):
         batch = 3 if L <= 18 else 1
         inp = synth.matvec_inputs(p, 1 << L, batch, seed=200 + L)
         c = run_matvec(inp)
-        check_sampled(inp, c, range(batch), count=1024 if L <= 20 else 512, thetas=2)
+        check_sampled(inp, c, range(batch), count=1024 if L <= 20 else (512 if L <= 22 else 256), thetas=2)
 
 
 def test_matvec_multipass_full_entries_2pow15():

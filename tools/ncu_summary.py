@@ -65,5 +65,43 @@ def full(path):
                 print(f"  {k} = {d[k]} {units[hdr.index(k)]}")
 
 
+UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1024, "MB": 1 << 20, "GB": 1 << 30}
+
+
+def traffic(path, kind, workload, kernel_regex, out_json="profiles/traffic.json"):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the kernels matching
+    kernel_regex in an ncu --set full report -> profiles/traffic.json[workload][kind]
+    (read by bench.py for the roofline "traffic" field)."""
+    import json
+    import os
+    import re
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    vals = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        if not re.search(kernel_regex, d.get("Kernel Name", "")):
+            continue
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            u = units[hdr.index(k)]
+            tot += float(d[k].replace(",", "")) * UNIT_SCALE.get(u, 1)
+        vals.append(tot)
+    if not vals:
+        raise SystemExit(f"no kernel matching {kernel_regex!r} in {path}")
+    db = json.load(open(out_json)) if os.path.exists(out_json) else {}
+    db.setdefault(workload, {})[kind] = {
+        "bytes_per_launch": sum(vals) / len(vals), "launches_captured": len(vals), "report": path,
+        "note": "ncu --set full (default --cache-control all: L2 flushed before each replay, so "
+                "intermediates the pipeline keeps in L2 are counted as DRAM reads)"}
+    json.dump(db, open(out_json, "w"), indent=1, sort_keys=True)
+    print(json.dumps(db[workload][kind]))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    cmd = sys.argv[1]
+    if cmd == "traffic":
+        traffic(*sys.argv[2:])
+    else:
+        {"launches": launches, "full": full}[cmd](sys.argv[2])
