@@ -147,6 +147,277 @@ struct FieldGoldSel {  // r01b variant (predicated corrections), kept for compar
   }
 };
 
+struct FieldGoldW {  // experiment: corrections via mad.wide with an opaque EPS register
+  uint32_t E = 0xFFFFFFFFu, NEG1 = 0xFFFFFFFFu;
+  using T = uint64_t;
+  using Tw = uint64_t;
+  static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
+  static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
+
+  // All helpers work on 32-bit halves with explicit PTX carry chains.  A wrap-around correction
+  // (+-EPS when a 64-bit add/sub carried/borrowed) is applied arithmetically, never by setp /
+  // selp / predication: after a subtract chain `subc.u32 m, 0, 0` yields m = -borrow (0 or
+  // 0xffffffff = EPS's low word) and the correction is one more subtract chain; after an add
+  // chain `addc.u32 m, 0, 0` yields the carry and `mad.lo.cc m * EPS` adds the correction.  (PTX
+  // carry flags are the hardware carry: after an add, `subc m, 0, 0` gives carry - 1, NOT -carry,
+  // so add and subtract chains are never mixed.)  ptxas maps the materialisations to IMAD.X /
+  // IMAD on the FMA pipe, which offloads the saturated ALU pipe
+  // (profiles/r01c_ncu_full_k_block.txt: the predicated form spent ~11 SEL/ISETP/PLOP3 per modmul).
+  __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+  __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+  // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS;
+  // a + b - 2^64 + EPS <= (2^64-1) + (p-1) - 2^64 + EPS = 2^64 - 2: no second carry.  Weak result.
+  __device__ __forceinline__ uint64_t add_c(uint64_t a, uint64_t b) const {
+    uint64_t r;
+    asm("{\n\t.reg .u32 s0, s1, k;\n\t"
+        "add.cc.u32  s0, %1, %3;\n\t"
+        "addc.cc.u32 s1, %2, %4;\n\t"
+        "addc.u32    k, 0, 0;\n\t"
+        "mov.b64     %0, {s0, s1};\n\t"
+        "mad.wide.u32 %0, k, %5, %0;\n\t"
+        "}"
+        : "=l"(r) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)), "r"(E));
+    return r;
+  }
+  // a - b mod p for a any 64-bit value and b < p: on a borrow subtract EPS; the wrapped value is
+  // a - b + 2^64 >= 2^64 - p + 1 > EPS, so no second borrow.  Canonical if a is canonical.
+  __device__ __forceinline__ static uint64_t sub_c(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"        // m = -borrow
+        "sub.cc.u32  %0, %0, m;\n\t"      // - EPS
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // a - b mod p for any 64-bit a, b: up to two borrow corrections (the second only if
+  // b > a + p - 2^64 + EPS, i.e. both were large); result a - b + {0, p, 2p}, weakly reduced.
+  __device__ __forceinline__ static uint64_t sub_w(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.cc.u32 %1, %1, 0;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
+  //   V = (t1:t0) + t2 EPS - t3 as a 3-word signed value c 2^64 + (r1:r0), c in {-1, 0, 1}
+  //       (V in (-2^32, 2^65 - 2^33]);
+  //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
+  //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
+  //   canonicalise: u = r + EPS carries iff r >= p; then r += EPS * carry (mod 2^64) = r - p.
+  __device__ __forceinline__ uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) const {
+    uint64_t r;
+    asm("{\n\t.reg .u32 r0, r1, c, k, m;\n\t"
+        "mad.lo.cc.u32   r0, %3, 0xffffffff, %1;\n\t"
+        "madc.hi.cc.u32  r1, %3, 0xffffffff, %2;\n\t"
+        "addc.u32        c, 0, 0;\n\t"
+        "sub.cc.u32      r0, r0, %4;\n\t"
+        "subc.cc.u32     r1, r1, 0;\n\t"
+        "subc.u32        c, c, 0;\n\t"
+        "mov.b64         %0, {r0, r1};\n\t"
+        "mad.wide.s32    %0, c, %6, %0;\n\t"      // r - c
+        "mov.b64         {r0, r1}, %0;\n\t"
+        "add.u32         r1, r1, c;\n\t"          // + c 2^32: r + c EPS
+        "add.cc.u32      m, r0, 0xffffffff;\n\t"  // carry iff r >= p
+        "addc.cc.u32     m, r1, 0;\n\t"
+        "addc.u32        k, 0, 0;\n\t"
+        "mov.b64         %0, {r0, r1};\n\t"
+        "mad.wide.u32    %0, k, %5, %0;\n\t"  // r + EPS k (mod 2^64) = r - p k
+        "}"
+        : "=l"(r) : "r"(t0), "r"(t1), "r"(t2), "r"(t3), "r"(E), "r"(NEG1));
+    return r;
+  }
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  __device__ __forceinline__ uint64_t mul(uint64_t a, uint64_t b) const {
+    // ptxas expands mul.lo.u64 / mul.hi.u64 into IMAD.WIDE.U32 chains with carry predicates
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
+
+  // forward a: inputs weak; t = s y canonical -> single corrections
+  __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(y, s);
+    const uint64_t X = x;
+    x = add_c(X, t);
+    y = sub_c(X, t);
+  }
+  // forward b: t = s x canonical; t + y single correction; t - y with weak y needs two
+  __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(x, s);
+    const uint64_t Y = y;
+    x = add_c(Y, t);
+    y = sub_w(t, Y);
+  }
+  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
+  __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
+    const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
+    const uint64_t d = sub_c(u, v);   // canonical
+    u = mul(s, si);
+    v = d;
+  }
+  __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
+    const uint64_t s = add_c(u, v);
+    const uint64_t d = sub_c(u, v);
+    u = mul(s, si_k);
+    v = mul(d, k);
+  }
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
+    return mul(mul(a, b), k);
+  }
+};
+
+struct FieldGoldW2 {  // experiment: W + FMA-pipe borrow corrections + opaque-zero carry materialisation
+  uint32_t E = 0xFFFFFFFFu, NEG1 = 0xFFFFFFFFu, Z = 0u;
+  using T = uint64_t;
+  using Tw = uint64_t;
+  static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
+  static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
+
+  // All helpers work on 32-bit halves with explicit PTX carry chains.  A wrap-around correction
+  // (+-EPS when a 64-bit add/sub carried/borrowed) is applied arithmetically, never by setp /
+  // selp / predication: after a subtract chain `subc.u32 m, 0, 0` yields m = -borrow (0 or
+  // 0xffffffff = EPS's low word) and the correction is one more subtract chain; after an add
+  // chain `addc.u32 m, 0, 0` yields the carry and `mad.lo.cc m * EPS` adds the correction.  (PTX
+  // carry flags are the hardware carry: after an add, `subc m, 0, 0` gives carry - 1, NOT -carry,
+  // so add and subtract chains are never mixed.)  ptxas maps the materialisations to IMAD.X /
+  // IMAD on the FMA pipe, which offloads the saturated ALU pipe
+  // (profiles/r01c_ncu_full_k_block.txt: the predicated form spent ~11 SEL/ISETP/PLOP3 per modmul).
+  __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+  __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+  // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS;
+  // a + b - 2^64 + EPS <= (2^64-1) + (p-1) - 2^64 + EPS = 2^64 - 2: no second carry.  Weak result.
+  __device__ __forceinline__ uint64_t add_c(uint64_t a, uint64_t b) const {
+    uint64_t r;
+    asm("{\n\t.reg .u32 s0, s1, k;\n\t"
+        "add.cc.u32  s0, %1, %3;\n\t"
+        "addc.cc.u32 s1, %2, %4;\n\t"
+        "addc.u32    k, %6, %6;\n\t"
+        "mov.b64     %0, {s0, s1};\n\t"
+        "mad.wide.u32 %0, k, %5, %0;\n\t"
+        "}"
+        : "=l"(r) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)), "r"(E), "r"(Z));
+    return r;
+  }
+  // a - b mod p for a any 64-bit value and b < p: on a borrow subtract EPS; the wrapped value is
+  // a - b + 2^64 >= 2^64 - p + 1 > EPS, so no second borrow.  Canonical if a is canonical.
+  __device__ __forceinline__ uint64_t sub_c(uint64_t a, uint64_t b) const {
+    uint64_t r;
+    asm("{\n\t.reg .u32 d0, d1, m;\n\t"
+        "sub.cc.u32  d0, %1, %3;\n\t"
+        "subc.cc.u32 d1, %2, %4;\n\t"
+        "subc.u32    m, 0, 0;\n\t"             // m = -borrow
+        "mov.b64     %0, {d0, d1};\n\t"
+        "mad.wide.s32 %0, m, %5, %0;\n\t"     // r + borrow   (m * -1)
+        "mov.b64     {d0, d1}, %0;\n\t"
+        "add.u32     d1, d1, m;\n\t"          // - borrow 2^32: r - borrow EPS
+        "mov.b64     %0, {d0, d1};\n\t"
+        "}"
+        : "=l"(r) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)), "r"(NEG1));
+    return r;
+  }
+  // a - b mod p for any 64-bit a, b: up to two borrow corrections (the second only if
+  // b > a + p - 2^64 + EPS, i.e. both were large); result a - b + {0, p, 2p}, weakly reduced.
+  __device__ __forceinline__ static uint64_t sub_w(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.cc.u32 %1, %1, 0;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
+  //   V = (t1:t0) + t2 EPS - t3 as a 3-word signed value c 2^64 + (r1:r0), c in {-1, 0, 1}
+  //       (V in (-2^32, 2^65 - 2^33]);
+  //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
+  //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
+  //   canonicalise: u = r + EPS carries iff r >= p; then r += EPS * carry (mod 2^64) = r - p.
+  __device__ __forceinline__ uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) const {
+    uint64_t r;
+    asm("{\n\t.reg .u32 r0, r1, c, k, m;\n\t"
+        "mad.lo.cc.u32   r0, %3, 0xffffffff, %1;\n\t"
+        "madc.hi.cc.u32  r1, %3, 0xffffffff, %2;\n\t"
+        "addc.u32        c, %7, %7;\n\t"
+        "sub.cc.u32      r0, r0, %4;\n\t"
+        "subc.cc.u32     r1, r1, 0;\n\t"
+        "subc.u32        c, c, 0;\n\t"
+        "mov.b64         %0, {r0, r1};\n\t"
+        "mad.wide.s32    %0, c, %6, %0;\n\t"      // r - c
+        "mov.b64         {r0, r1}, %0;\n\t"
+        "add.u32         r1, r1, c;\n\t"          // + c 2^32: r + c EPS
+        "add.cc.u32      m, r0, 0xffffffff;\n\t"  // carry iff r >= p
+        "addc.cc.u32     m, r1, 0;\n\t"
+        "addc.u32        k, %7, %7;\n\t"
+        "mov.b64         %0, {r0, r1};\n\t"
+        "mad.wide.u32    %0, k, %5, %0;\n\t"  // r + EPS k (mod 2^64) = r - p k
+        "}"
+        : "=l"(r) : "r"(t0), "r"(t1), "r"(t2), "r"(t3), "r"(E), "r"(NEG1), "r"(Z));
+    return r;
+  }
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  __device__ __forceinline__ uint64_t mul(uint64_t a, uint64_t b) const {
+    // ptxas expands mul.lo.u64 / mul.hi.u64 into IMAD.WIDE.U32 chains with carry predicates
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
+
+  // forward a: inputs weak; t = s y canonical -> single corrections
+  __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(y, s);
+    const uint64_t X = x;
+    x = add_c(X, t);
+    y = sub_c(X, t);
+  }
+  // forward b: t = s x canonical; t + y single correction; t - y with weak y needs two
+  __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(x, s);
+    const uint64_t Y = y;
+    x = add_c(Y, t);
+    y = sub_w(t, Y);
+  }
+  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
+  __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
+    const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
+    const uint64_t d = sub_c(u, v);   // canonical
+    u = mul(s, si);
+    v = d;
+  }
+  __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
+    const uint64_t s = add_c(u, v);
+    const uint64_t d = sub_c(u, v);
+    u = mul(s, si_k);
+    v = mul(d, k);
+  }
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
+    return mul(mul(a, b), k);
+  }
+};
+
 }  // namespace fcirc
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { fprintf(stderr, "CUDA %s line %d\n", cudaGetErrorString(e_), __LINE__); return 1; } } while (0)
@@ -164,9 +435,22 @@ __device__ __forceinline__ uint64_t ref_sub(uint64_t a, uint64_t b) {
 
 constexpr int CH = 8, IT = 1024;
 
+// runtime-opaque constants (the library passes them in the field struct, a kernel argument)
+template <class FG> __device__ __forceinline__ void opaque(FG&, uint64_t) {}
+template <> __device__ __forceinline__ void opaque<FieldGoldW>(FieldGoldW& f, uint64_t s) {
+  f.E = 0xFFFFFFFFu ^ (uint32_t)(s >> 62);
+  f.NEG1 = f.E;
+}
+template <> __device__ __forceinline__ void opaque<FieldGoldW2>(FieldGoldW2& f, uint64_t s) {
+  f.E = 0xFFFFFFFFu ^ (uint32_t)(s >> 62);
+  f.NEG1 = f.E;
+  f.Z = (uint32_t)(s >> 62);
+}
+
 template <class FG, int KIND>
 __global__ void __launch_bounds__(256) k_tp(uint64_t* out, uint64_t seed) {
   FG F;
+  opaque(F, seed);
   uint64_t x[CH], y[CH];
   for (int c = 0; c < CH; ++c) { x[c] = seed * (threadIdx.x + 1) + c * 0x9E3779B97F4A7C15ull; y[c] = x[c] ^ 0xDEADBEEFCAFEF00Dull; }
   const uint64_t w = 0x1234567890ABCDEFull ^ seed;
@@ -188,6 +472,7 @@ __global__ void __launch_bounds__(256) k_tp(uint64_t* out, uint64_t seed) {
 template <class FG>
 __global__ void k_check(unsigned long long* bad, uint64_t seed) {
   FG F;
+  opaque(F, seed);
   const uint64_t edge[] = {0, 1, 2, P - 1, P, P + 1, 0xFFFFFFFFFFFFFFFFull, 0xFFFFFFFF00000000ull,
                            0x00000000FFFFFFFFull, 0x8000000000000000ull, 0xFFFFFFFEFFFFFFFFull, P - 2};
   uint64_t s = seed ^ (threadIdx.x + blockIdx.x * 977ull);
@@ -255,5 +540,7 @@ int main() {
   int nsm; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
   int rc = run<FieldGoldSel>("r01b predicated corrections (FieldGoldSel)", nsm);
   rc |= run<FieldGold>("mask corrections (FieldGold, current)", nsm);
+  rc |= run<FieldGoldW>("mad.wide corrections (FieldGoldW)", nsm);
+  rc |= run<FieldGoldW2>("W + FMA borrow corrections + opaque zero (FieldGoldW2)", nsm);
   return rc;
 }
