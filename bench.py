@@ -5,7 +5,9 @@ A "step" is one batched f-circulant matrix-vector product (the whole hot path of
 forward split of a and b, leaves, recombination, 1/n scaling) over one batch of synthetic input.
 Default workload = the BASELINE.json metric point (SURVEY §8(d) C4 @ n=2^20): Goldilocks
 p = 2^64-2^32+1, n = 2^20, batch 64, f = w^n (seeded), a, b ~ U[0,p) — 512 MiB per operand, so
-every step reads its inputs from HBM (inputs larger than the 126 MB L2).
+every step reads its inputs from HBM (inputs larger than the 126 MB L2).  --config selects the
+other configurations: S1 / C2 / C4 sweep points (matvec), C3 (polynomial products, step = one
+batched fcirc_polymul) and C5 (big integers, step = one batched bigint_mul).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fcirc|reference] [--config NAME]
 
@@ -47,22 +49,35 @@ SM_MHZ = 1965.0
 MODMUL_PER_CLK_SM = {"u64": 8.0, "u32": 16.0}
 PRIMITIVE_MEASURED_PER_CLK_SM = {"u64": 3.16, "u32": 15.98}  # profiles/r01_peaks.jsonl (gold64 / shoup32)
 HBM_GBS_FALLBACK = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+MMAX = {"u64": 12, "u32": 13}  # on-chip sub-problem size (matvec_impl.cuh FTraits::MMAX)
 
 WORKLOADS = {
-    "C4_n20": dict(cfg="C4_n20", desc="C4 @ n=2^20: Goldilocks f-circulant matvec, batch 64, f=w^n"),
-    "S1": dict(cfg="S1", desc="S1: p=998244353 f-circulant matvec n=2^20, batch 64, f=w^n"),
-    "C2_f1": dict(cfg="C2_f1", desc="C2: p=998244353 circulant matvec n=2^12, batch 4096, f=1"),
-    "C2_fm1": dict(cfg="C2_fm1", desc="C2: p=998244353 negacyclic matvec n=2^12, batch 4096, f=p-1"),
-    **{f"C4_n{L}": dict(cfg=f"C4_n{L}", desc=f"C4 @ n=2^{L}: Goldilocks f-circulant matvec, batch 2^{26 - L}")
+    "C4_n20": "C4 @ n=2^20: Goldilocks f-circulant matvec, batch 64, f=w^n",
+    "S1": "S1: p=998244353 f-circulant matvec n=2^20, batch 64, f=w^n",
+    "C1": "C1: p=998244353 f-circulant matvec n=2^10, batch 1, f=w^n",
+    "C2_f1": "C2: p=998244353 circulant matvec n=2^12, batch 4096, f=1",
+    "C2_fm1": "C2: p=998244353 negacyclic matvec n=2^12, batch 4096, f=p-1",
+    **{f"C4_n{L}": f"C4 @ n=2^{L}: Goldilocks f-circulant matvec, batch 2^{26 - L}"
        for L in range(12, 23) if L != 20},
+    "C3": "C3: polynomial products mod 998244353, 2^20 x 2^20 coefficients -> 2^21 circulant (f=1), batch 16",
+    "C5": "C5: 2^22-bit integer products, 16-bit limbs, 3 primes x 2^19 circulant (f=1) + CRT + carry, batch 8",
 }
-MMAX = {"u64": 12, "u32": 13}  # fcirc_max_fused_log2 (matvec_impl.cuh FTraits::MMAX)
 
 
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             return json.load(fh)
+    except Exception:
+        return None
+
+
+def traffic_record(config: str, kind: str):
+    """DRAM bytes per launch of `kind` from the committed ncu --set full capture (profiles/traffic.json,
+    written by tools/ncu_summary.py traffic), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get(config, {}).get(kind)
     except Exception:
         return None
 
@@ -182,22 +197,150 @@ def algorithmic_modmuls(kind: str, n: int, batch: int, width: str) -> float:
     return 0.0
 
 
-def cpu_oracle_rate(inp, seconds: float = 3.0, instance: int = 0):
-    """Time the oracle (as it stands) on a bounded sample: entries of one instance, O(n) each."""
-    import oracle
-    p, f, n = inp["p"], inp["f"], inp["n"]
-    threads = oracle.default_threads()
-    a, b = inp["a"][instance], inp["b"][instance]
-    probe = max(threads, 32)
-    t0 = time.perf_counter()
-    oracle.fcirc_entries(p, f, a, b, np.arange(probe, dtype=np.int64))
-    dt = time.perf_counter() - t0
-    count = int(min(n, max(probe, probe * seconds / max(dt, 1e-6))))
-    idx = np.random.default_rng(7).integers(0, n, count).astype(np.int64)
-    t0 = time.perf_counter()
-    oracle.fcirc_entries(p, f, a, b, idx)
-    dt = time.perf_counter() - t0
-    return count / dt, count, dt, threads
+def cfg_dtype(p: int) -> str:
+    return "u64" if p >= (1 << 32) else "u32"
+
+
+def next_pow2(x: int) -> int:
+    r = 1
+    while r < x:
+        r <<= 1
+    return r
+
+
+class Workload:
+    """One benchmark configuration: inputs, the step through the public API, its end-to-end
+    (host buffers) variant, the elements it counts and the oracle sample of the CPU baseline."""
+
+    def __init__(self, name: str, rank: int = 0):
+        self.name, self.desc = name, WORKLOADS[name]
+        cfg = dict(synth.CONFIGS[name])
+        self.kind = cfg.pop("kind")
+        self.cfg = rank_config(cfg, rank)
+        if self.kind == "matvec":
+            self.inp = synth.matvec_inputs(**self.cfg)
+            self.p, self.n, self.batch = self.inp["p"], self.inp["n"], self.inp["batch"]
+            self.width = cfg_dtype(self.p)
+            self.elems = self.batch * self.n                 # output entries
+            self.mm_n, self.mm_batch = self.n, self.batch    # matvec instances launched per step
+        elif self.kind == "polymul":
+            self.inp = synth.polymul_inputs(**self.cfg)
+            self.p, self.batch = self.inp["p"], self.inp["batch"]
+            self.n = next_pow2(self.inp["na"] + self.inp["nb"] - 1)
+            self.width = cfg_dtype(self.p)
+            self.elems = self.batch * self.n                 # circulant entries (SURVEY §8(d) C3)
+            self.mm_n, self.mm_batch = self.n, self.batch
+        elif self.kind == "bigint":
+            self.inp = synth.bigint_inputs(**self.cfg)
+            self.p, self.batch = synth.P998, self.inp["batch"]
+            nw = self.inp["nwords"]
+            self.n = next_pow2(2 * (nw + nw) - 1)
+            self.width = "u32"
+            self.elems = self.batch * self.n                 # output limb positions (SURVEY §8(d) C5)
+            self.mm_n, self.mm_batch = self.n, 3 * self.batch  # three primes
+        else:
+            raise ValueError(self.kind)
+
+    # ---------------------------------------------------------------- device side
+    def setup(self, torch, fc):
+        self.torch, self.fc = torch, fc
+        i = self.inp
+        if self.kind == "matvec":
+            self.dev = [torch.from_numpy(i["a"]).cuda(), torch.from_numpy(i["b"]).cuda()]
+            self.out = torch.empty_like(self.dev[0])
+        elif self.kind == "polymul":
+            self.dev = [torch.from_numpy(i["a"]).cuda(), torch.from_numpy(i["b"]).cuda()]
+            self.out = torch.empty((self.batch, i["na"] + i["nb"] - 1), dtype=self.dev[0].dtype, device="cuda")
+        else:
+            self.dev = [torch.from_numpy(i["x"]).cuda(), torch.from_numpy(i["y"]).cuda()]
+            self.out = torch.empty((self.batch, 2 * i["nwords"]), dtype=self.dev[0].dtype, device="cuda")
+
+    def step(self):
+        fc, (x, y) = self.fc, self.dev
+        if self.kind == "matvec":
+            fc.matvec(x, y, self.inp["f"], self.p, out=self.out)
+        elif self.kind == "polymul":
+            fc.polymul(x, y, self.p, out=self.out)
+        else:
+            fc.bigint_mul(x, y, out=self.out)
+        return fc.last_launch_count()
+
+    # ---------------------------------------------------------------- end to end (host buffers)
+    def setup_host(self):
+        torch = self.torch
+        self.host = [torch.from_numpy(np.ascontiguousarray(a)).pin_memory() for a in self._host_arrays()]
+        self.host_out = torch.empty(tuple(self.out.shape), dtype=self.out.dtype).pin_memory()
+        self.h2d_bytes = sum(h.numel() * h.element_size() for h in self.host)
+        self.d2h_bytes = self.host_out.numel() * self.host_out.element_size()
+
+    def _host_arrays(self):
+        i = self.inp
+        return (i["a"], i["b"]) if self.kind in ("matvec", "polymul") else (i["x"], i["y"])
+
+    def host_step(self):
+        """One step through the public API from pinned host memory (H2D, product, D2H)."""
+        if self.kind == "matvec":
+            self.fc.matvec_host(self.host[0], self.host[1], self.inp["f"], self.p, out=self.host_out)
+            return "fcirc_matvec_host (pinned host buffers, chunk-pipelined H2D / kernels / D2H)"
+        torch = self.torch
+        for d, h in zip(self.dev, self.host):
+            d.copy_(h, non_blocking=True)
+        self.step()
+        self.host_out.copy_(self.out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return ("pinned host -> device copies, fcirc_%s, device -> pinned host copy, synchronize"
+                % ("polymul" if self.kind == "polymul" else "bigint_mul"))
+
+    # ---------------------------------------------------------------- CPU oracle sample
+    def cpu_sample(self, seconds: float, step_index: int = 0):
+        """(elements/s, count, seconds, threads, description) of the oracle as it stands on a
+        bounded sample of this workload (entries / coefficients / whole products)."""
+        import oracle
+        threads = oracle.default_threads()
+        i = self.inp
+        k = step_index % self.batch
+        if self.kind == "bigint":
+            t0 = time.perf_counter()
+            reps = 0
+            while True:
+                oracle.bigint_mul(i["x"][k], i["y"][k])
+                reps += 1
+                if time.perf_counter() - t0 >= seconds * 0.5 or reps >= 64:
+                    break
+            dt = time.perf_counter() - t0
+            return (reps * self.n / dt, reps * self.n, dt, 1,
+                    f"{reps} full products of instance {k} (independent Karatsuba on 32-bit words, "
+                    f"one thread); counted as {self.n} output limb positions each")
+        if self.kind == "polymul":
+            fn = lambda ks: oracle.polymul_coeffs(self.p, i["a"][k], i["b"][k], ks)  # noqa: E731
+            what = "schoolbook coefficients"
+            total = i["na"] + i["nb"] - 1
+        else:
+            fn = lambda ks: oracle.fcirc_entries(self.p, self.inp["f"], i["a"][k], i["b"][k], ks)  # noqa: E731
+            what = "output entries (Definition 2, O(n) multiply-adds each)"
+            total = self.n
+        probe = max(threads, 32)
+        t0 = time.perf_counter()
+        fn(np.arange(probe, dtype=np.int64))
+        dt = time.perf_counter() - t0
+        count = int(min(total, max(probe, probe * seconds / max(dt, 1e-6))))
+        idx = np.random.default_rng(7 + step_index).integers(0, total, count).astype(np.int64)
+        t0 = time.perf_counter()
+        fn(idx)
+        dt = time.perf_counter() - t0
+        return (count / dt, count, dt, threads,
+                f"{count} seeded-random {what} of instance {k} of {self.desc}; {dt:.1f} s wall")
+
+    def config_block(self, args):
+        arr = self._host_arrays()[0]
+        blk = {"workload": self.desc, "p": int(self.p), "n": int(self.n), "batch": int(self.batch),
+               "l2": ("inputs larger than L2 (%.0f MiB per input operand per rank; L2 126 MB)" % (arr.nbytes / 2**20)
+                      if arr.nbytes > (126 << 20) else
+                      "inputs smaller than L2 (%.1f MiB per operand); no flush between steps" % (arr.nbytes / 2**20)),
+               "parallelism": f"replicas x{args.gpus} (independent instances per GPU, no collective)"}
+        if self.kind == "matvec":
+            blk["f"] = "w^n" if self.inp.get("w") not in (None, 1) else ("1" if self.inp["f"] == 1 else "p-1")
+        return blk
 
 
 # ------------------------------------------------------------------------------------ arms
@@ -206,49 +349,27 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    w = WORKLOADS[args.config]
-    cfg = {k: v for k, v in synth.CONFIGS[w["cfg"]].items() if k != "kind"}
-    inp = synth.matvec_inputs(**cfg)
-    n = inp["n"]
-    import oracle
-    threads = oracle.default_threads()
-    # each step: a bounded sample of the workload (entries of one instance), ~1 s of wall time
-    rate, count, dt, _ = cpu_oracle_rate(inp, seconds=0.5)
-    per_step = max(threads, int(rate * 1.0))
-    times = []
+    wl = Workload(args.config)
+    _, _, _, threads, _ = wl.cpu_sample(0.2)
+    times, counts, desc = [], [], ""
     for s in range(args.warmup + args.steps):
-        k = s % inp["batch"]
-        idx = np.random.default_rng(100 + s).integers(0, n, per_step).astype(np.int64)
-        t0 = time.perf_counter()
-        oracle.fcirc_entries(inp["p"], inp["f"], inp["a"][k], inp["b"][k], idx)
+        rate, count, dt, threads, desc = wl.cpu_sample(1.0, step_index=s)
         if s >= args.warmup:
-            times.append(time.perf_counter() - t0)
+            times.append(dt)
+            counts.append(count)
     total = sum(times)
-    value = per_step * len(times) / total / 1e9
-    sample = (f"{per_step} seeded-random output entries per step of one instance (step s -> instance s mod "
-              f"{inp['batch']}) of {w['desc']}; Definition 2 written out, O(n) multiply-adds per entry")
+    value = sum(counts) / total / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": cfg_dtype(inp["p"]),
-        "data": "synthetic", "config": config_block(args, inp, w),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": wl.width,
+        "data": "synthetic", "config": wl.config_block(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": "per step: " + desc.rsplit(";", 1)[0] + " (about 1 s of CPU work per step)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
-
-
-def cfg_dtype(p: int) -> str:
-    return "u64" if p >= (1 << 32) else "u32"
-
-
-def config_block(args, inp, w):
-    return {"workload": w["desc"], "p": int(inp["p"]), "n": int(inp["n"]), "batch": int(inp["batch"]),
-            "f": "w^n" if inp.get("w") not in (None, 1) else ("1" if inp["f"] == 1 else "p-1"),
-            "l2": "inputs larger than L2 (a, b, c each %.0f MiB per rank; L2 126 MB)" %
-                  (inp["a"].nbytes / 2**20),
-            "parallelism": f"replicas x{args.gpus} (independent instances per GPU, no collective)"}
 
 
 def run_fcirc(args):
@@ -262,23 +383,17 @@ def run_fcirc(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    w = WORKLOADS[args.config]
-    cfg = {k: v for k, v in synth.CONFIGS[w["cfg"]].items() if k != "kind"}
-    inp = synth.matvec_inputs(**rank_config(cfg, rank))
-    p, f, n, batch = inp["p"], inp["f"], inp["n"], inp["batch"]
-    width = cfg_dtype(p)
-    a = torch.from_numpy(inp["a"]).cuda()
-    b = torch.from_numpy(inp["b"]).cuda()
-    c = torch.empty_like(a)
+    wl = Workload(args.config, rank)
+    wl.setup(torch, fc)
     stream = torch.cuda.current_stream()
 
-    # plan build (first call) timed separately
+    # plan build (first call) timed separately, then the remaining warm-up steps
     t0 = time.perf_counter()
-    fc.matvec(a, b, f, p, out=c)
+    wl.step()
     torch.cuda.synchronize()
     plan_ms = 1000 * (time.perf_counter() - t0)
-    for _ in range(max(args.warmup - 1, 2)):
-        fc.matvec(a, b, f, p, out=c)
+    for _ in range(args.warmup - 1):
+        wl.step()
     torch.cuda.synchronize()
 
     # ---- timed region (device time, CUDA events on the launching stream)
@@ -292,8 +407,7 @@ def run_fcirc(args):
     with sampler:
         ev0.record(stream)
         for _ in range(args.steps):
-            fc.matvec(a, b, f, p, out=c)
-            launches += fc.last_launch_count()
+            launches += wl.step()
         ev1.record(stream)
         torch.cuda.synchronize()
     fc.profile_enable(False)
@@ -303,9 +417,10 @@ def run_fcirc(args):
     ms = ev0.elapsed_time(ev1)
     ms_max = max_over_ranks(ms, world)
     ms_step = ms_max / args.steps
-    value = whole_job_gelems(world, batch, n, args.steps, ms_max)
+    value = world * wl.elems * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel
+    width, n, batch = wl.width, wl.mm_n, wl.mm_batch
     dom = max((k for k in prof if prof[k][0] > 0), key=lambda k: prof[k][1])
     cnt, kms = prof[dom]
     per_launch_mm = algorithmic_modmuls(dom, n, batch, width) * args.steps / cnt
@@ -318,45 +433,43 @@ def run_fcirc(args):
     step_mm = batch * n * (1.5 * L + 1)
     step_bytes = 3 * batch * n * (8 if width == "u64" else 4)
     t_roof = max(step_bytes / (hbm * 1e9), step_mm / (peak * 1e12))
+    tr = traffic_record(args.config, dom)
     roofline = {
         "bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "Tmodmul/s",
-        "frac": achieved / peak, "traffic": None,
+        "frac": achieved / peak, "traffic": tr["bytes_per_launch"] if tr else None,
+        "traffic_source": (f"{tr['report']} ({tr['note']})" if tr else None),
         "per_launch": {"modmuls": per_launch_mm, "avg_ms": avg_ms, "launches": cnt},
         "peak_derivation": f"{SMS} SMs x {SM_MHZ:.0f} MHz x {MODMUL_PER_CLK_SM[width]:.0f} modmul/clk/SM "
-                           f"(minimal FMA-pipe slots per modmul, DESIGN.md §6)",
+                           f"(minimal FMA-pipe slots per modmul, DESIGN.md §6); of derived peak",
         "primitive_microbench_tmodmul_s": SMS * SM_MHZ * 1e6 * PRIMITIVE_MEASURED_PER_CLK_SM[width] / 1e12,
         "kernel_share_of_step": kms / ms,
         "kernels": {k: {"launches": v[0], "ms_total": v[1]} for k, v in prof.items() if v[0]},
         "step": {"t_roof_ms": 1000 * t_roof, "frac": 1000 * t_roof / ms_step,
                  "hbm_bound_ms": 1000 * step_bytes / (hbm * 1e9), "alu_bound_ms": 1000 * step_mm / (peak * 1e12),
-                 "hbm_gbs_peak": hbm, "hbm_gbs_achieved_alg": step_bytes / (ms_step * 1e-3) / 1e9},
+                 "hbm_gbs_peak": hbm, "hbm_peak_source": "MEASURED_PEAKS.json hbm_gbs" if mp else "fallback",
+                 "hbm_gbs_achieved_alg": step_bytes / (ms_step * 1e-3) / 1e9},
     }
 
-    # ---- end to end through the public host API (pinned host buffers, H2D + kernels + D2H)
+    # ---- end to end through the public API (pinned host buffers, H2D + product + D2H per step)
     e2e = None
     if not args.no_e2e:
-        ha = torch.from_numpy(inp["a"]).pin_memory()
-        hb = torch.from_numpy(inp["b"]).pin_memory()
-        hc = torch.empty_like(ha).pin_memory()
-        fc.matvec_host(ha, hb, f, p, out=hc)
+        wl.setup_host()
+        api = wl.host_step()
         if world > 1:
             dist.barrier()
         e_steps = max(1, min(args.steps, args.e2e_steps))
         t0 = time.perf_counter()
         for _ in range(e_steps):
-            fc.matvec_host(ha, hb, f, p, out=hc)
+            wl.host_step()
         dt = max_over_ranks(time.perf_counter() - t0, world)
-        esz = 8 if width == "u64" else 4
-        e2e = {"value": world * batch * n * e_steps / dt / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * batch * n * esz, "d2h_bytes_per_step": batch * n * esz,
-               "steps": e_steps, "api": "fcirc_matvec_host (pinned host buffers; wall clock, synchronous call)"}
+        e2e = {"value": world * wl.elems * e_steps / dt / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": wl.h2d_bytes, "d2h_bytes_per_step": wl.d2h_bytes,
+               "steps": e_steps, "api": api + "; wall clock, max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rate, count, dt, threads = cpu_oracle_rate(inp, seconds=args.cpu_seconds)
-        cpu = {"value": rate / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"{count} seeded-random output entries of instance 0 of {w['desc']} "
-                         f"(Definition 2, O(n) multiply-adds each); {dt:.1f} s wall"}
+        rate, count, dt, threads, desc = wl.cpu_sample(args.cpu_seconds)
+        cpu = {"value": rate / 1e9, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": desc}
 
     if world > 1:
         dist.barrier()
@@ -365,7 +478,7 @@ def run_fcirc(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": width, "data": "synthetic (seeded uniform residues, SURVEY §8(d))",
-            "config": config_block(args, inp, w), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "config": wl.config_block(args), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": sampler.summary(), "plan_build_ms": plan_ms,
         }
         print(json.dumps(line), flush=True)

@@ -29,7 +29,7 @@ namespace fcirc {
 // ------------------------------------------------------------------------------------------
 // 32-bit NTT primes
 // ------------------------------------------------------------------------------------------
-struct TwU32 {
+struct __align__(8) TwU32 {  // 8-byte aligned: one 64-bit load per twiddle
   uint32_t w, q;  // twiddle and its Shoup quotient floor(w * 2^32 / p)
 };
 
