@@ -16,6 +16,7 @@
 
 #include "../../include/fcirc.h"
 #include "apps.cuh"
+#include "fcirc_kernels.cuh"
 #include "plan.h"
 #include "runtime.h"
 
@@ -178,7 +179,27 @@ static int ilog2_exact(int64_t n) {
   return L;
 }
 
-// fcirc_matvec without resetting the launch counter (used by the applications as well)
+// plan lookup + dispatch of one batched product (no argument validation; callers validate)
+static int matvec_core(uint64_t p, uint64_t f, const void* a, const void* b, void* c, int L, int64_t batch,
+                       cudaStream_t st, const EmbedIO& io) {
+  const PrimeInfo* pi = prime_info(p);
+  if (!pi) return FCIRC_EPRIME;
+  if (L > pi->two_adicity || L > max_log_n(pi->wide)) return FCIRC_ESIZE;
+  // Theorem 1 premises (P:52) checked on the host before touching the device
+  if (f % p == 0 || powmod(f % p, (p - 1) >> L, p) != 1) return FCIRC_ENOROOT;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
+  std::shared_ptr<DevPlan> dp;
+  int rc = get_plan(dev, p, f % p, L, &dp);
+  if (rc) return rc;
+  if (pi->wide) {
+    FieldGold fld;
+    return run_matvec_gold(fld, *dp, a, b, c, L, batch, st, dev, io);
+  }
+  return run_matvec_u32(make_u32(p), *dp, a, b, c, L, batch, st, dev, io);
+}
+
+// fcirc_matvec without resetting the launch counter (also used by the host pipeline)
 static int matvec_impl(uint64_t p, uint64_t f, const void* a, const void* b, void* c, int64_t n, int64_t batch,
                        cudaStream_t st) {
   if (!a || !b || !c || n < 1 || batch < 1) return FCIRC_EINVAL;
@@ -190,18 +211,7 @@ static int matvec_impl(uint64_t p, uint64_t f, const void* a, const void* b, voi
   if (L > pi->two_adicity || L > max_log_n(pi->wide)) return FCIRC_ESIZE;
   const size_t bytes = (size_t)n * (size_t)batch * es;
   if (overlaps(c, bytes, a, bytes) || overlaps(c, bytes, b, bytes)) return FCIRC_EINVAL;
-  // Theorem 1 premises (P:52) checked on the host before touching the device
-  if (f % p == 0 || powmod(f % p, (p - 1) >> L, p) != 1) return FCIRC_ENOROOT;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
-  std::shared_ptr<DevPlan> dp;
-  int rc = get_plan(dev, p, f % p, L, &dp);
-  if (rc) return rc;
-  if (pi->wide) {
-    FieldGold fld;
-    return run_matvec_gold(fld, *dp, a, b, c, L, batch, st, dev);
-  }
-  return run_matvec_u32(make_u32(p), *dp, a, b, c, L, batch, st, dev);
+  return matvec_core(p, f, a, b, c, L, batch, st, EmbedIO{});
 }
 
 static int64_t next_pow2(int64_t x) {
@@ -210,37 +220,16 @@ static int64_t next_pow2(int64_t x) {
   return r;
 }
 
-// polynomial product through an f = 1 circulant of order L; a~ embedding (R8)
-template <class E>
-static int polymul_impl(uint64_t p, const E* a, int64_t na, const E* b, int64_t nb, E* c, int64_t batch,
-                        cudaStream_t st, int tag) {
-  const int64_t nc = na + nb - 1;
-  const int64_t L = next_pow2(nc);
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
-  void* ws;
-  int rc = get_workspace(dev, (void*)st, (size_t)(3 * batch * L) * sizeof(E), &ws, tag);
-  if (rc) return rc;
-  E* at = (E*)ws;
-  E* bp = at + batch * L;
-  E* cf = bp + batch * L;
-  const int64_t tot = batch * L;
-  const int thr = 256;
-  const int64_t blocks = std::min<int64_t>((tot + thr - 1) / thr, 148 * 16);
-  prof_begin(4, st);
-  k_embed<E><<<(unsigned)blocks, thr, 0, st>>>(a, na, b, nb, at, bp, L, batch);
-  prof_end(st);
-  ++g_launches;
-  if (cudaPeekAtLastError() != cudaSuccess) return FCIRC_ECUDA;
-  rc = matvec_impl(p, 1, at, bp, cf, L, batch, st);
-  if (rc) return rc;
-  const int64_t totc = batch * nc;
-  const int64_t blocks2 = std::min<int64_t>((totc + thr - 1) / thr, 148 * 16);
-  prof_begin(4, st);
-  k_truncate<E><<<(unsigned)blocks2, thr, 0, st>>>(cf, L, c, nc, batch);
-  prof_end(st);
-  ++g_launches;
-  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+// polynomial product through an f = 1 circulant of order L (reading R8): the
+// a~ embedding is fused into the first pass's loads and the truncation into the last pass's stores
+static int polymul_impl(uint64_t p, const void* a, int64_t na, const void* b, int64_t nb, void* c, int64_t batch,
+                        cudaStream_t st) {
+  EmbedIO io;
+  io.mode = EMB_POLY;
+  io.na = na;
+  io.nb = nb;
+  io.nc = na + nb - 1;
+  return matvec_core(p, 1, a, b, c, ilog2_exact(next_pow2(io.nc)), batch, st, io);
 }
 
 // host buffers -> device -> host, pipelined over NSLOT streams (fcirc_matvec_host)
@@ -303,32 +292,40 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   if (ilog2_exact(L) > 23) return FCIRC_ESIZE;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
-  const size_t need = (size_t)(5 * batch * L) * 4 + (size_t)(2 * batch * ncoef) * 8 + (size_t)(batch * nd) * 4;
+  const int64_t nseg = (nd + kCarrySeg - 1) / kCarrySeg;
+  const size_t need = (size_t)(3 * batch * L) * 4 + (size_t)(2 * batch * ncoef) * 8 + (size_t)(batch * nd) * 4 +
+                      (size_t)(batch * nseg) * 4;
   void* ws;
   int rc = get_workspace(dev, (void*)st, need, &ws, 2);
   if (rc) return rc;
-  uint32_t* at = (uint32_t*)ws;
-  uint32_t* bp = at + batch * L;
-  uint32_t* r1 = bp + batch * L;
+  uint32_t* r1 = (uint32_t*)ws;
   uint32_t* r2 = r1 + batch * L;
   uint32_t* r3 = r2 + batch * L;
   uint64_t* V = (uint64_t*)(r3 + batch * L);
   uint32_t* E = (uint32_t*)(V + 2 * batch * ncoef);
+  uint32_t* S = E + batch * nd;
   const int thr = 256;
   auto nblk = [&](int64_t tot) { return (unsigned)std::min<int64_t>((tot + thr - 1) / thr, 148 * 16); };
-  prof_begin(4, st);
-  k_bigint_embed<<<nblk(batch * L), thr, 0, st>>>(x, nx, y, ny, at, bp, L, batch);
-  prof_end(st);
-  ++g_launches;
-  if (cudaPeekAtLastError() != cudaSuccess) return FCIRC_ECUDA;
-  if ((rc = matvec_impl(P1, 1, at, bp, r1, L, batch, st))) return rc;
-  if ((rc = matvec_impl(P2, 1, at, bp, r2, L, batch, st))) return rc;
-  if ((rc = matvec_impl(P3, 1, at, bp, r3, L, batch, st))) return rc;
+  // 16-bit limb split + a~ embedding fused into the first pass of each product (EMB_LIMBS)
+  EmbedIO io;
+  io.mode = EMB_LIMBS;
+  io.na = nx;
+  io.nb = ny;
+  const int lg = ilog2_exact(L);
+  if ((rc = matvec_core(P1, 1, x, y, r1, lg, batch, st, io))) return rc;
+  if ((rc = matvec_core(P2, 1, x, y, r2, lg, batch, st, io))) return rc;
+  if ((rc = matvec_core(P3, 1, x, y, r3, lg, batch, st, io))) return rc;
   GarnerConsts g;
-  g.p1 = P1; g.p2 = P2; g.p3 = P3;
-  g.inv_p1_mod_p2 = invmod(P1 % P2, P2);
-  g.p1p2_mod_p3 = mulmod(P1 % P3, P2 % P3, P3);
-  g.inv_p1p2_mod_p3 = invmod(g.p1p2_mod_p3, P3);
+  g.p1 = (uint32_t)P1; g.p2 = (uint32_t)P2; g.p3 = (uint32_t)P3;
+  g.p1p2 = P1 * P2;
+  g.one2q = (uint32_t)((1ull << 32) / P2);
+  g.one3q = (uint32_t)((1ull << 32) / P3);
+  g.c12 = (uint32_t)invmod(P1 % P2, P2);
+  g.c12q = (uint32_t)(((uint64_t)g.c12 << 32) / P2);
+  g.p1m3 = (uint32_t)(P1 % P3);
+  g.p1m3q = (uint32_t)(((uint64_t)g.p1m3 << 32) / P3);
+  g.c123 = (uint32_t)invmod(mulmod(P1 % P3, P2 % P3, P3), P3);
+  g.c123q = (uint32_t)(((uint64_t)g.c123 << 32) / P3);
   prof_begin(4, st);
   k_garner<<<nblk(batch * ncoef), thr, 0, st>>>(r1, r2, r3, L, ncoef, batch, g, V);
   prof_end(st);
@@ -338,9 +335,15 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   prof_end(st);
   ++g_launches;
   prof_begin(4, st);
-  k_carry<<<(unsigned)batch, kCarryThreads, 0, st>>>(E, nd, z, nx + ny, nullptr);
+  k_carry_seg<<<(unsigned)(batch * nseg), kCarryThreads, 0, st>>>(E, nd, nseg, S);
   prof_end(st);
-  ++g_launches;
+  prof_begin(4, st);
+  k_carry_top<<<(unsigned)batch, 32, 0, st>>>(S, nseg, batch);
+  prof_end(st);
+  prof_begin(4, st);
+  k_carry_apply<<<(unsigned)(batch * nseg), kCarryThreads, 0, st>>>(E, nd, nseg, S, z, nx + ny);
+  prof_end(st);
+  g_launches += 3;
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
 
@@ -395,10 +398,7 @@ int fcirc_polymul(uint64_t p, const void* a, int64_t na, const void* b, int64_t 
     return FCIRC_EINVAL;
   const int64_t L = next_pow2(nc);
   if (ilog2_exact(L) > pi->two_adicity || ilog2_exact(L) > max_log_n(pi->wide)) return FCIRC_ESIZE;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (pi->wide)
-    return polymul_impl<uint64_t>(p, (const uint64_t*)a, na, (const uint64_t*)b, nb, (uint64_t*)c, batch, st, 1);
-  return polymul_impl<uint32_t>(p, (const uint32_t*)a, na, (const uint32_t*)b, nb, (uint32_t*)c, batch, st, 1);
+  return polymul_impl(p, a, na, b, nb, c, batch, (cudaStream_t)stream);
 }
 
 const char* fcirc_strerror(int status) {

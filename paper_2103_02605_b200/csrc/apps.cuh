@@ -1,98 +1,61 @@
 // apps.cuh — kernels of the applications built on the f-circulant product.
 //
-//   k_embed / k_truncate  polynomial product as an f = 1 circulant: the row is the
-//                         index-reversed, zero-padded a~ (a~[0] = a[0], a~[L-m] = a[m]) so that
-//                         (A(a~) b)_i = sum_j a[(i-j) mod L] b_j, the cyclic convolution, which
-//                         equals the linear one because L >= na + nb - 1 (reading R8).
+// The polynomial embedding (row a~, zero padding, truncation) and the big-integer limb
+// split are fused into the first / last pass of the product itself (fcirc_kernels.cuh EmbedIO).
+// What remains here is the tail of the big-integer product (reading R12):
+// Garner CRT of the three residues, 16-bit digit sums and the carry propagation.
 #pragma once
 #include <cstdint>
 
 namespace fcirc {
 
-template <class E>
-__global__ void k_embed(const E* __restrict__ a, int64_t na, const E* __restrict__ b, int64_t nb,
-                        E* __restrict__ at, E* __restrict__ bp, int64_t L, int64_t batch) {
-  const int64_t tot = batch * L;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t inst = i / L, pos = i - inst * L;
-    E va = 0;
-    if (pos == 0) va = a[inst * na];
-    else if (pos >= L - (na - 1)) va = a[inst * na + (L - pos)];
-    at[i] = va;
-    bp[i] = pos < nb ? b[inst * nb + pos] : (E)0;
-  }
-}
-
-template <class E>
-__global__ void k_truncate(const E* __restrict__ cf, int64_t L, E* __restrict__ c, int64_t nc, int64_t batch) {
-  const int64_t tot = batch * nc;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t inst = i / nc, k = i - inst * nc;
-    c[i] = cf[inst * L + k];
-  }
-}
-
-}  // namespace fcirc
-
-// ------------------------------------------------------------------------------------------
-// large integers, reading R12: 16-bit limbs, three f = 1 circulant
-// products mod 998244353 / 469762049 / 167772161, Garner CRT, carry propagation.
-// ------------------------------------------------------------------------------------------
-namespace fcirc {
-
-__device__ __forceinline__ uint32_t limb16(const uint32_t* w, int64_t m) {
-  return (w[m >> 1] >> (16 * (m & 1))) & 0xFFFFu;
-}
-
-// at = limb-row of x in the a~ embedding, bp = zero-padded limbs of y (limbs < 2^16 < every p)
-__global__ void k_bigint_embed(const uint32_t* __restrict__ x, int64_t nx, const uint32_t* __restrict__ y,
-                               int64_t ny, uint32_t* __restrict__ at, uint32_t* __restrict__ bp, int64_t L,
-                               int64_t batch) {
-  const int64_t tot = batch * L, lx = 2 * nx, ly = 2 * ny;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t inst = i / L, pos = i - inst * L;
-    const uint32_t* xi = x + inst * nx;
-    uint32_t va = 0;
-    if (pos == 0) va = limb16(xi, 0);
-    else if (pos >= L - (lx - 1)) va = limb16(xi, L - pos);
-    at[i] = va;
-    bp[i] = pos < ly ? limb16(y + inst * ny, pos) : 0u;
-  }
-}
-
 struct GarnerConsts {
-  uint64_t p1, p2, p3;
-  uint64_t inv_p1_mod_p2;      // p1^-1 mod p2
-  uint64_t inv_p1p2_mod_p3;    // (p1 p2)^-1 mod p3
-  uint64_t p1p2_mod_p3;
+  uint32_t p1, p2, p3;
+  uint64_t p1p2;             // p1 p2 (< 2^59)
+  uint32_t one2q, one3q;     // floor(2^32 / p2), floor(2^32 / p3): reduce a 32-bit value (Shoup, w = 1)
+  uint32_t c12, c12q;        // p1^-1 mod p2 (Shoup pair)
+  uint32_t p1m3, p1m3q;      // p1 mod p3
+  uint32_t c123, c123q;      // (p1 p2)^-1 mod p3
 };
 
-// V_k = CRT(r1, r2, r3) as a 128-bit integer (< p1 p2 p3 < 2^85), stored as two u64 words
+// x w mod p for x < 2^32, with the Shoup quotient wq = floor(w 2^32 / p); canonical result
+__device__ __forceinline__ uint32_t shoup_red(uint32_t x, uint32_t w, uint32_t wq, uint32_t p) {
+  const uint32_t r = x * w - __umulhi(x, wq) * p;   // in [0, 2p)
+  return r >= p ? r - p : r;
+}
+__device__ __forceinline__ uint32_t sub_mod(uint32_t a, uint32_t b, uint32_t p) { return a >= b ? a - b : a + p - b; }
+__device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) {
+  const uint32_t s = a + b;
+  return s >= p ? s - p : s;
+}
+
+// V_k = CRT(r1, r2, r3) for one coefficient (Garner, mixed radix p1, p1 p2):
+//   v1 = r1,  v2 = (r2 - v1) p1^-1 mod p2,  v3 = (r3 - v1 - v2 p1) (p1 p2)^-1 mod p3,
+//   V = v1 + v2 p1 + v3 p1 p2 < p1 p2 p3 < 2^85, stored as (low 64 bits, high bits).
+// (Within bigint_mul's size limit every coefficient is < 2^54 < p1 p2, so v3 = 0; the general
+// three-prime reconstruction is kept as BASELINE.json's C5 route prescribes.)
 __global__ void k_garner(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2,
                          const uint32_t* __restrict__ r3, int64_t L, int64_t ncoef, int64_t batch, GarnerConsts g,
                          uint64_t* __restrict__ V) {
   const int64_t tot = batch * ncoef;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t inst = i / ncoef, k = i - inst * ncoef;
-    const uint64_t a1 = r1[inst * L + k], a2 = r2[inst * L + k], a3 = r3[inst * L + k];
-    const uint64_t v1 = a1;
-    const uint64_t v2 = ((a2 + g.p2 - (v1 % g.p2)) % g.p2) * g.inv_p1_mod_p2 % g.p2;
-    // (a3 - v1 - v2 p1) mod p3
-    const uint64_t t = (v1 % g.p3 + (v2 % g.p3) * (g.p1 % g.p3)) % g.p3;
-    const uint64_t v3 = ((a3 + g.p3 - t) % g.p3) * g.inv_p1p2_mod_p3 % g.p3;
+    const uint32_t v1 = r1[inst * L + k];
+    const uint32_t v2 = shoup_red(sub_mod(r2[inst * L + k], shoup_red(v1, 1u, g.one2q, g.p2), g.p2), g.c12, g.c12q, g.p2);
+    const uint32_t t = add_mod(shoup_red(v1, 1u, g.one3q, g.p3), shoup_red(v2, g.p1m3, g.p1m3q, g.p3), g.p3);
+    const uint32_t v3 = shoup_red(sub_mod(r3[inst * L + k], t, g.p3), g.c123, g.c123q, g.p3);
     const unsigned __int128 val = (unsigned __int128)v1 + (unsigned __int128)v2 * g.p1 +
-                                  (unsigned __int128)v3 * ((unsigned __int128)g.p1 * g.p2);
+                                  (unsigned __int128)v3 * g.p1p2;
     V[2 * i] = (uint64_t)val;
     V[2 * i + 1] = (uint64_t)(val >> 64);
   }
 }
 
 __device__ __forceinline__ uint32_t chunk16(const uint64_t* V, int64_t k, int i) {
-  const uint64_t w = V[2 * k + (i >> 2)];
-  return (uint32_t)(w >> (16 * (i & 3))) & 0xFFFFu;
+  return (uint32_t)(V[2 * k + (i >> 2)] >> (16 * (i & 3))) & 0xFFFFu;
 }
 
-// D_j = sum_{i<6} chunk_i(V_{j-i})  (< 6 * 2^16);  E_j = (D_j mod 2^16) + floor(D_{j-1} / 2^16)  (< 2^17)
+// D_j = sum_{i<6} chunk_i(V_{j-i})  (< 6 * 2^16);  E_j = (D_j mod 2^16) + floor(D_{j-1} / 2^16)  (< 2^16 + 6)
 __global__ void k_digits(const uint64_t* __restrict__ V, int64_t ncoef, int64_t nd, int64_t batch,
                          uint32_t* __restrict__ Eo) {
   const int64_t tot = batch * nd;
@@ -109,55 +72,113 @@ __global__ void k_digits(const uint64_t* __restrict__ V, int64_t ncoef, int64_t 
   }
 }
 
-// carry-lookahead over E_j = e_j + g_j 2^16 (g_j in {0,1}): carry_out = g | (p & carry_in),
-// p = (e == 0xFFFF).  One CTA per integer; thread-sequential chunks + block scan of (g, p).
-constexpr int kCarryThreads = 1024;
-__global__ void __launch_bounds__(kCarryThreads)
-k_carry(const uint32_t* __restrict__ E, int64_t nd, uint32_t* __restrict__ z, int64_t nw, int* __restrict__ overflow) {
-  const int64_t inst = blockIdx.x;
-  const uint32_t* Ei = E + inst * nd;
-  uint32_t* zi = z + inst * nw;
-  const int64_t per = (nd + kCarryThreads - 1) / kCarryThreads;
-  const int64_t j0 = threadIdx.x * per, j1 = min(nd, j0 + per);
-  // local (g, p) of this chunk, composed left to right
-  uint32_t G = 0, Pp = 1;
-  for (int64_t j = j0; j < j1; ++j) {
-    const uint32_t e = Ei[j];
-    const uint32_t g = e >> 16, p = (e & 0xFFFFu) == 0xFFFFu;
-    G = g | (p & G);
-    Pp = Pp & p;
+// ------------------------------------------------------------------------------------------
+// carry propagation: E_j = e_j + g_j 2^16 with g_j in {0, 1}; digit j absorbs the carry c_j,
+// c_{j+1} = g_j | (p_j & c_j), p_j = (e_j == 0xFFFF).  (G, P) pairs compose associatively
+// (earlier segment X, later Y): (G_Y | (P_Y & G_X), P_Y & P_X).  Three launches:
+//   k_carry_seg   per (integer, segment of kCarrySeg digits): the segment's (G, P)
+//   k_carry_top   per integer: exclusive scan over its segments -> carry into each segment
+//   k_carry_apply per (integer, segment): block scan with the carry-in, write 32-bit words
+// Each thread owns kCarryPer consecutive digits (coalesced uint4 loads).
+// ------------------------------------------------------------------------------------------
+constexpr int kCarryThreads = 256;
+constexpr int kCarryPer = 8;
+constexpr int kCarrySeg = kCarryThreads * kCarryPer;   // 2048 digits = 1024 output words
+
+struct GP { uint32_t g, p; };
+__device__ __forceinline__ GP gp_compose(GP x, GP y) { return {y.g | (y.p & x.g), y.p & x.p}; }  // x then y
+
+// block-wide exclusive scan of (G, P) (identity (0, 1)); returns this thread's prefix, *total
+__device__ __forceinline__ GP gp_block_exscan(GP v, GP* total) {
+  __shared__ uint32_t wg[kCarryThreads / 32], wp[kCarryThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  GP inc = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    GP o{__shfl_up_sync(0xffffffffu, inc.g, off), __shfl_up_sync(0xffffffffu, inc.p, off)};
+    if (lane >= off) inc = gp_compose(o, inc);
   }
-  // exclusive scan across threads (carry into each chunk)
-  __shared__ uint32_t sg[kCarryThreads], sp[kCarryThreads];
-  sg[threadIdx.x] = G;
-  sp[threadIdx.x] = Pp;
+  if (lane == 31) { wg[warp] = inc.g; wp[warp] = inc.p; }
   __syncthreads();
-  for (int off = 1; off < kCarryThreads; off <<= 1) {
-    uint32_t g2 = 0, p2 = 1;
-    if ((int)threadIdx.x >= off) { g2 = sg[threadIdx.x - off]; p2 = sp[threadIdx.x - off]; }
-    __syncthreads();
-    // (earlier block) then (this prefix): g = g_this | (p_this & g_earlier)
-    const uint32_t gt = sg[threadIdx.x], pt = sp[threadIdx.x];
-    sg[threadIdx.x] = gt | (pt & g2);
-    sp[threadIdx.x] = pt & p2;
-    __syncthreads();
-  }
-  uint32_t cin = threadIdx.x == 0 ? 0u : sg[threadIdx.x - 1];
-  for (int64_t j = j0; j < j1; ++j) {
-    const uint32_t e = Ei[j];
-    const uint32_t s = (e & 0xFFFFu) + cin;
-    const uint32_t d = s & 0xFFFFu;
-    cin = (e >> 16) | (s >> 16);
-    // digits j -> word j/2 (16-bit halves); each word is written by the thread owning its low digit
-    if (j & 1) continue;
-    uint32_t hi = 0;
-    if (j + 1 < nd) {
-      const uint32_t e1 = Ei[j + 1];
-      hi = ((e1 & 0xFFFFu) + cin) & 0xFFFFu;
+  GP wpre{0u, 1u};
+  for (int w = 0; w < warp; ++w) wpre = gp_compose(wpre, GP{wg[w], wp[w]});
+  GP tot{0u, 1u};
+  for (int w = 0; w < kCarryThreads / 32; ++w) tot = gp_compose(tot, GP{wg[w], wp[w]});
+  *total = tot;
+  GP ex{__shfl_up_sync(0xffffffffu, inc.g, 1), __shfl_up_sync(0xffffffffu, inc.p, 1)};
+  if (lane == 0) ex = GP{0u, 1u};
+  return gp_compose(wpre, ex);
+}
+
+__device__ __forceinline__ void load_digits(const uint32_t* Ei, int64_t nd, int64_t j0, uint32_t e[kCarryPer]) {
+#pragma unroll
+  for (int q = 0; q < kCarryPer; ++q) e[q] = (j0 + q < nd) ? Ei[j0 + q] : 0u;
+}
+
+__device__ __forceinline__ GP local_gp(const uint32_t e[kCarryPer]) {
+  GP acc{0u, 1u};
+#pragma unroll
+  for (int q = 0; q < kCarryPer; ++q) acc = gp_compose(acc, GP{e[q] >> 16, (e[q] & 0xFFFFu) == 0xFFFFu});
+  return acc;
+}
+
+__global__ void __launch_bounds__(kCarryThreads)
+k_carry_seg(const uint32_t* __restrict__ E, int64_t nd, int64_t nseg, uint32_t* __restrict__ seg_gp) {
+  const int64_t inst = blockIdx.x / nseg, sg = blockIdx.x - inst * nseg;
+  const int64_t j0 = sg * kCarrySeg + (int64_t)threadIdx.x * kCarryPer;
+  uint32_t e[kCarryPer];
+  load_digits(E + inst * nd, nd, j0, e);
+  GP tot;
+  gp_block_exscan(local_gp(e), &tot);
+  if (threadIdx.x == 0) seg_gp[blockIdx.x] = tot.g | (tot.p << 1);
+}
+
+// one warp per integer: carry into every segment (exclusive scan of the segment pairs)
+__global__ void k_carry_top(uint32_t* __restrict__ seg_gp, int64_t nseg, int64_t batch) {
+  const int64_t inst = blockIdx.x;
+  if (inst >= batch) return;
+  uint32_t* s = seg_gp + inst * nseg;
+  const int lane = threadIdx.x;
+  uint32_t carry = 0;   // carry into the current 32-segment window
+  for (int64_t w0 = 0; w0 < nseg; w0 += 32) {
+    const int64_t i = w0 + lane;
+    const uint32_t v = i < nseg ? s[i] : 2u;   // identity (g = 0, p = 1)
+    GP inc{v & 1u, v >> 1};
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      GP o{__shfl_up_sync(0xffffffffu, inc.g, off), __shfl_up_sync(0xffffffffu, inc.p, off)};
+      if (lane >= off) inc = gp_compose(o, inc);
     }
-    if ((j >> 1) < nw) zi[j >> 1] = d | (hi << 16);
+    GP ex{__shfl_up_sync(0xffffffffu, inc.g, 1), __shfl_up_sync(0xffffffffu, inc.p, 1)};
+    if (lane == 0) ex = GP{0u, 1u};
+    const uint32_t cin = ex.g | (ex.p & carry);
+    const uint32_t last_g = __shfl_sync(0xffffffffu, inc.g, 31), last_p = __shfl_sync(0xffffffffu, inc.p, 31);
+    __syncwarp();
+    if (i < nseg) s[i] = cin;   // overwrite with the carry into segment i
+    carry = last_g | (last_p & carry);
   }
-  if (overflow && threadIdx.x == kCarryThreads - 1 && cin) atomicExch(overflow, 1);
+}
+
+__global__ void __launch_bounds__(kCarryThreads)
+k_carry_apply(const uint32_t* __restrict__ E, int64_t nd, int64_t nseg, const uint32_t* __restrict__ seg_cin,
+              uint32_t* __restrict__ z, int64_t nw) {
+  const int64_t inst = blockIdx.x / nseg, sg = blockIdx.x - inst * nseg;
+  const int64_t j0 = sg * kCarrySeg + (int64_t)threadIdx.x * kCarryPer;
+  uint32_t e[kCarryPer];
+  load_digits(E + inst * nd, nd, j0, e);
+  GP tot;
+  const GP pre = gp_block_exscan(local_gp(e), &tot);
+  uint32_t c = pre.g | (pre.p & seg_cin[blockIdx.x]);   // carry into this thread's first digit
+  uint32_t* zi = z + inst * nw;
+#pragma unroll
+  for (int q = 0; q < kCarryPer; q += 2) {
+    const uint32_t s0 = (e[q] & 0xFFFFu) + c;
+    c = (e[q] >> 16) | (s0 >> 16);
+    const uint32_t s1 = (e[q + 1] & 0xFFFFu) + c;
+    c = (e[q + 1] >> 16) | (s1 >> 16);
+    const int64_t w = (j0 + q) >> 1;
+    if (w < nw) zi[w] = (s0 & 0xFFFFu) | ((s1 & 0xFFFFu) << 16);
+  }
 }
 
 }  // namespace fcirc

@@ -27,14 +27,17 @@ namespace fcirc {
 __host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
 
 // Phase geometry of a 2^NB-point transform done by threads holding R = 2^r points each.
-// Phase 0 covers the top r address bits, the last phase the lowest rp_last bits.
+// Phase 0 covers the top rp(0) = NB - r (NPH - 1) address bits (the short phase when r does not
+// divide NB), every later phase r bits, the last one the lowest r.  Putting the short phase on top
+// keeps every low phase a full r bits wide, which is what makes the smem swizzle below
+// conflict-free in every phase (the top phase is contiguous across threads anyway).
 template <int NB, int R>
 struct Phases {
   static constexpr int r = ilog2c(R);
   static constexpr int T = (1 << NB) / R;            // threads per transform
   static constexpr int NPH = NB == 0 ? 0 : (NB + r - 1) / r;
-  static __host__ __device__ constexpr int rp(int ph) { return ph < NPH - 1 ? r : NB - r * (NPH - 1); }
-  static __host__ __device__ constexpr int lo(int ph) { return NB - r * ph - rp(ph); }
+  static __host__ __device__ constexpr int rp(int ph) { return ph == 0 ? NB - r * (NPH - 1) : r; }
+  static __host__ __device__ constexpr int lo(int ph) { return NB - rp(0) - r * ph; }
   // runtime part of the address of thread t in phase ph (bits of t spread around the phase bits)
   static __device__ __forceinline__ int ins_t(int ph, int t) {
     const int l = lo(ph), w = rp(ph);
@@ -49,15 +52,64 @@ struct Phases {
   }
 };
 
-template <class T>
-struct PadOf;
-template <>
-struct PadOf<uint32_t> { static constexpr int SH = 5; };  // one pad word per 32 words
-template <>
-struct PadOf<uint64_t> { static constexpr int SH = 4; };  // one pad element per 16 elements
+// Shared-memory swizzle of the phase exchanges: address x -> x ^ ((x >> r) & MASK), a GF(2)-linear
+// bijection (so swz(a | b) = swz(a) ^ swz(b) for disjoint bit fields).  In a phase whose slot bits
+// sit at [lo, lo + r), the thread bits above them are folded back onto the bank bits, so the 32
+// threads of a warp (16 per wavefront for 8-byte elements) hit distinct banks in every phase
+// (model: tools/bank_model.py; ncu: profiles/r01c_ncu_full_k_block_C4n20.txt had 25% conflicts
+// with the former one-pad-per-16/32-elements layout).
+template <class T> struct SwzMask;
+template <> struct SwzMask<uint32_t> { static constexpr int V = 31; };  // 32 banks of 4 bytes
+template <> struct SwzMask<uint64_t> { static constexpr int V = 15; };  // 16 8-byte lanes per wavefront
+
+template <int R, class T>
+__host__ __device__ __forceinline__ constexpr int swz(int x) {
+  return x ^ ((x >> ilog2c(R)) & SwzMask<T>::V);
+}
+
+// ------------------------------------------------------------------------------------------
+// Input/output modes of the first and last pass (embeddings fused into the loads,
+// truncation into the stores, so the applications read no zero padding and write no scratch):
+//   EMB_PLAIN   a, b, c are [batch][n] (fcirc_matvec)
+//   EMB_POLY    polynomial product through an f = 1 circulant of order n (DESIGN.md
+//               reading R8): row a~[0] = a[0], a~[pos] = a[n - pos] for pos > n - na, else 0;
+//               vector b zero-padded; c truncated to nc = na + nb - 1 coefficients.
+//   EMB_LIMBS   big integers: a, b are [batch][na | nb] little-endian 32-bit words read
+//               as 16-bit limbs (row = reversed limbs of a, vector = limbs of b); c is [batch][n].
+// ------------------------------------------------------------------------------------------
+enum { EMB_PLAIN = 0, EMB_POLY = 1, EMB_LIMBS = 2 };
+struct EmbedIO {
+  int mode = EMB_PLAIN;
+  int64_t na = 0, nb = 0;   // EMB_POLY: coefficients per instance; EMB_LIMBS: 32-bit words
+  int64_t nc = 0;           // EMB_POLY: output coefficients per instance
+};
 
 template <class T>
-__device__ __forceinline__ int padi(int x) { return x + (x >> PadOf<T>::SH); }
+__device__ __forceinline__ T limb_at(const T* w, int64_t m) {
+  if constexpr (sizeof(T) == 4) return (w[m >> 1] >> (16 * (m & 1))) & 0xFFFFu;
+  else return 0;  // limbs are only used with the 32-bit primes
+}
+// element `pos` of the row (second = false) or the vector (second = true) of instance `inst`
+template <class T>
+__device__ __forceinline__ T io_load(const T* src, int64_t inst, int64_t pos, int64_t n, bool second, const EmbedIO& io) {
+  if (io.mode == EMB_PLAIN) return src[inst * n + pos];
+  if (io.mode == EMB_POLY) {
+    if (second) return pos < io.nb ? src[inst * io.nb + pos] : (T)0;
+    const T* ai = src + inst * io.na;
+    return pos == 0 ? ai[0] : (pos > n - io.na ? ai[n - pos] : (T)0);
+  }
+  if (second) return pos < 2 * io.nb ? limb_at(src + inst * io.nb, pos) : (T)0;
+  const T* xi = src + inst * io.na;
+  return pos == 0 ? limb_at(xi, 0) : (pos > n - 2 * io.na ? limb_at(xi, n - pos) : (T)0);
+}
+template <class T>
+__device__ __forceinline__ void io_store(T* dst, int64_t inst, int64_t pos, int64_t n, T v, const EmbedIO& io) {
+  if (io.mode == EMB_POLY) {
+    if (pos < io.nc) dst[inst * io.nc + pos] = v;
+  } else {
+    dst[inst * n + pos] = v;
+  }
+}
 
 // ------------------------------------------------------------------------------------------
 // k_block: fused sub-problem kernel
@@ -68,14 +120,16 @@ struct BlockArgs {
   const typename F::T* b;   // b'
   typename F::T* out;       // M (k > 0) or c (k == 0); may alias a
   int64_t units;            // batch * 2^k
-  int k;                    // levels above this kernel (0: whole problem)
+  int k;                    // levels above this kernel (0: whole problem); grid = 2^k x
+                            // ceil(batch / IPC), CTA b: sub-block E = b mod 2^k, instances (b >> k) IPC + li
   const typename F::Tw* twf;  // heap-indexed s_{d,e}
   const typename F::Tw* twi;  // heap-indexed s_{d,e}^-1
   typename F::Tw last_si;   // s_{0,0}^-1 * K   (used when k == 0)
   typename F::Tw last_k;    // K = n^-1 (x R for FieldU32)
+  EmbedIO io;               // k == 0 and EMB only: embedding of the loads / truncation of the stores
 };
 
-template <class F, int M, int R, int IPC, int MINB = 1>
+template <class F, int M, int R, int IPC, int MINB = 1, bool EMB = false>
 __global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
 k_block(F fld, BlockArgs<F> args) {
   using T = typename F::T;
@@ -84,30 +138,38 @@ k_block(F fld, BlockArgs<F> args) {
   constexpr int m = 1 << M;
   constexpr int TT = PH::T;
   constexpr int NPH = PH::NPH;
-  constexpr int PM = m + (m >> PadOf<T>::SH) + 1;  // padded length of one array in smem
+  constexpr int PM = m;  // length of one array in smem (swizzled, unpadded)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
 
   const int t = threadIdx.x % TT;
   const int li = threadIdx.x / TT;
-  const int64_t unit = (int64_t)blockIdx.x * IPC + li;
-  const bool active = unit < args.units;
   T* sa = sm + (size_t)li * 2 * PM;
   T* sb = sa + PM;
 
   const int k = args.k;
-  const int E = (int)(unit & ((1 << k) - 1));
+  const int E = (int)(blockIdx.x & ((1u << k) - 1));   // sub-block index
+  const int64_t batch = args.units >> k;
   const int gbase = ((1 << k) + E) << M;   // heap-extended address base (fits: < 2n <= 2^24)
-  const int64_t base = unit * m;
+  const int64_t inst = (int64_t)(blockIdx.x >> k) * IPC + li;
+  const bool active = inst < batch;
+  const int64_t base = ((inst << k) + E) * m;
 
   T xa[R], xb[R];
   // ---- load (phase-0 addresses: slot s at s * 2^lo + t, coalesced across t)
-  if (active) {
+  if (active && !EMB) {
 #pragma unroll
     for (int s = 0; s < R; ++s) {
       const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
       xa[s] = args.a[base + ad];
       xb[s] = args.b[base + ad];
+    }
+  } else if (active) {
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
+      xa[s] = io_load(args.a, inst, ad, m, false, args.io);
+      xb[s] = io_load(args.b, inst, ad, m, true, args.io);
     }
   } else {
 #pragma unroll
@@ -121,7 +183,7 @@ k_block(F fld, BlockArgs<F> args) {
       const int wb = PH::ins_t(ph - 1, t);
 #pragma unroll
       for (int s = 0; s < R; ++s) {
-        const int ad = padi<T>(wb) + padi<T>(PH::cslot(ph - 1, s));
+        const int ad = swz<R, T>(wb) ^ swz<R, T>(PH::cslot(ph - 1, s));
         sa[ad] = xa[s];
         sb[ad] = xb[s];
       }
@@ -129,7 +191,7 @@ k_block(F fld, BlockArgs<F> args) {
       const int rb = PH::ins_t(ph, t);
 #pragma unroll
       for (int s = 0; s < R; ++s) {
-        const int ad = padi<T>(rb) + padi<T>(PH::cslot(ph, s));
+        const int ad = swz<R, T>(rb) ^ swz<R, T>(PH::cslot(ph, s));
         xa[s] = sa[ad];
         xb[s] = sb[ad];
       }
@@ -155,8 +217,11 @@ k_block(F fld, BlockArgs<F> args) {
 
   // ---- leaves: 1x1 products (the recursion bottom), same thread/slot layout
   if constexpr (M == 0) {
-    if (active) args.out[base] = fld.single(xa[0], xb[0], args.last_k);
-    return;
+    if (active) {
+      const T v = fld.single(xa[0], xb[0], args.last_k);
+      if constexpr (EMB) io_store(args.out, inst, 0, 1, v, args.io);
+      else args.out[base] = v;
+    }
   } else {
   T xm[R];
 #pragma unroll
@@ -169,11 +234,11 @@ k_block(F fld, BlockArgs<F> args) {
     if (ph < NPH - 1) {
       const int wb = PH::ins_t(ph + 1, t);
 #pragma unroll
-      for (int s = 0; s < R; ++s) sa[padi<T>(wb) + padi<T>(PH::cslot(ph + 1, s))] = xm[s];
+      for (int s = 0; s < R; ++s) sa[swz<R, T>(wb) ^ swz<R, T>(PH::cslot(ph + 1, s))] = xm[s];
       __syncthreads();
       const int rb = PH::ins_t(ph, t);
 #pragma unroll
-      for (int s = 0; s < R; ++s) xm[s] = sa[padi<T>(rb) + padi<T>(PH::cslot(ph, s))];
+      for (int s = 0; s < R; ++s) xm[s] = sa[swz<R, T>(rb) ^ swz<R, T>(PH::cslot(ph, s))];
       __syncthreads();
     }
     const int rp = PH::rp(ph), lo = PH::lo(ph);
@@ -198,9 +263,12 @@ k_block(F fld, BlockArgs<F> args) {
   }
 
   // ---- store (phase-0 addresses, coalesced)
-  if (active) {
+  if (active && (!EMB || args.io.mode != EMB_POLY)) {
 #pragma unroll
     for (int s = 0; s < R; ++s) args.out[base + PH::ins_t(0, t) + PH::cslot(0, s)] = xm[s];
+  } else if (active) {
+#pragma unroll
+    for (int s = 0; s < R; ++s) io_store(args.out, inst, PH::ins_t(0, t) + PH::cslot(0, s), m, xm[s], args.io);
   }
   }  // M > 0
 }
@@ -222,9 +290,10 @@ struct ColArgs {
   const typename F::Tw* twi;
   typename F::Tw last_si;
   typename F::Tw last_k;
+  EmbedIO io;                 // EMB only: forward embedding of the loads; inverse truncation of the stores
 };
 
-template <class F, int K, int R, int W, bool INV, int MINB = 1>
+template <class F, int K, int R, int W, bool INV, int MINB = 1, bool EMB = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols(F fld, ColArgs<F> args) {
   using T = typename F::T;
@@ -239,20 +308,30 @@ k_cols(F fld, ColArgs<F> args) {
   const int64_t unit = blockIdx.x;
   const int64_t inst = unit / args.colblocks;
   const int64_t cb = unit - inst * args.colblocks;
-  const int64_t base = inst * args.n + cb * W + c;
+  const int64_t col = cb * W + c;
+  const int64_t base = inst * args.n + col;
   const int64_t m = args.m;
   const bool second = (!INV) && blockIdx.y == 1;   // forward: y = 0 -> a, y = 1 -> b
   const T* src = second ? args.src1 : args.src0;
   T* dst = second ? args.dst1 : args.dst0;
 
-  auto sidx = [&](int row) { return (row + (row >> 4)) * W + c; };
+  // row swizzle (GF(2)-linear bijection of [0, 2^K)): with the short phase on top, the rows a warp
+  // touches in one access land in distinct banks in every phase (tools/bank_model.py)
+  auto sidx = [&](int row) { return (row ^ ((row >> PH::r) & 7)) * W + c; };
 
   T x[R];
   const int ph_first = INV ? NPH - 1 : 0;
   {
     const int rb = PH::ins_t(ph_first, t);
 #pragma unroll
-    for (int s = 0; s < R; ++s) x[s] = src[base + (int64_t)(rb + PH::cslot(ph_first, s)) * m];
+    if (INV || !EMB) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) x[s] = src[base + (int64_t)(rb + PH::cslot(ph_first, s)) * m];
+    } else {
+#pragma unroll
+      for (int s = 0; s < R; ++s)
+        x[s] = io_load(src, inst, col + (int64_t)(rb + PH::cslot(ph_first, s)) * m, args.n, second, args.io);
+    }
   }
 
   if (!INV) {
@@ -322,8 +401,13 @@ k_cols(F fld, ColArgs<F> args) {
       }
     }
     const int rb = PH::ins_t(0, t);
+    if (!EMB || args.io.mode != EMB_POLY) {
 #pragma unroll
-    for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(0, s)) * m] = x[s];
+      for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(0, s)) * m] = x[s];
+    } else {
+#pragma unroll
+      for (int s = 0; s < R; ++s) io_store(dst, inst, col + (int64_t)(rb + PH::cslot(0, s)) * m, args.n, x[s], args.io);
+    }
   }
 }
 

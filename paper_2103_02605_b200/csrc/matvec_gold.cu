@@ -4,8 +4,8 @@
 namespace fcirc {
 
 int run_matvec_gold(const FieldGold& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
-                    int64_t batch, cudaStream_t st, int dev) {
-  return run_matvec(fld, dp, a, b, c, L, batch, st, dev);
+                    int64_t batch, cudaStream_t st, int dev, const EmbedIO& io) {
+  return run_matvec(fld, dp, a, b, c, L, batch, st, dev, io);
 }
 
 int max_log_n(bool wide) { return (wide ? FTraits<FieldGold>::MMAX : FTraits<FieldU32>::MMAX) + KMAX; }

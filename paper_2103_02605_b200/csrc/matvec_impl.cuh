@@ -40,17 +40,17 @@ template <int RR> constexpr int wsel(int K) {
   return (256 * rsel<RR>(K)) >> K < 8 ? 8 : ((256 * rsel<RR>(K)) >> K);
 }
 
-template <class F, int M, int RR>
+template <class F, int M, int RR, bool EMB = false>
 static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
   constexpr int R = rsel<RR>(M), IPC = ipcsel<RR>(M);
   constexpr int T = (1 << M) / R;
   using E = typename F::T;
-  constexpr int PM = (1 << M) + ((1 << M) >> PadOf<E>::SH) + 1;
+  constexpr int PM = 1 << M;  // swizzled, unpadded (fcirc_kernels.cuh swz)
   const size_t smem = (size_t)IPC * 2 * PM * sizeof(E);
   // occupancy target: 1024 resident threads per SM for R <= 8 (register cap 64), 512 for R = 16
   // (cap 128: without a floor ptxas spends ~190 registers and halves the resident warps)
   constexpr int MINB = (T * IPC < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / (T * IPC) : 1;
-  auto kern = k_block<F, M, R, IPC, MINB>;
+  auto kern = k_block<F, M, R, IPC, MINB, EMB>;
   if (smem > 48 * 1024) {
     static bool once = false;  // attribute set per kernel instantiation
     if (!once) {
@@ -59,7 +59,8 @@ static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st)
       once = true;
     }
   }
-  const int64_t grid = (args.units + IPC - 1) / IPC;
+  const int64_t batch = args.units >> args.k;
+  const int64_t grid = ((batch + IPC - 1) / IPC) << args.k;
   prof_begin(args.k == 0 ? 0 : 1, st);
   kern<<<(unsigned)grid, T * IPC, smem, st>>>(fld, args);
   prof_end(st);
@@ -67,14 +68,14 @@ static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st)
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
 
-template <class F, int K, bool INV, int RR>
+template <class F, int K, bool INV, int RR, bool EMB = false>
 static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
   constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
   constexpr int threads = W * ((1 << K) / R);
   using E = typename F::T;
-  const size_t smem = (size_t)((1 << K) + ((1 << K) >> 4)) * W * sizeof(E);
+  const size_t smem = (size_t)(1 << K) * W * sizeof(E);
   constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
-  auto kern = k_cols<F, K, R, W, INV, MINB>;
+  auto kern = k_cols<F, K, R, W, INV, MINB, EMB>;
   if (smem > 48 * 1024) {
     static bool once = false;
     if (!once) {
@@ -104,6 +105,8 @@ template <> struct RDefault<FieldGold> { static constexpr int RB = 8, RC = 8; };
 
 template <class F, int M>
 static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
+  // the application embeddings (fused path only) use one variant: the default R
+  if (args.k == 0 && args.io.mode != EMB_PLAIN) return launch_block<F, M, RDefault<F>::RB, true>(fld, args, st);
   if constexpr (M >= FTraits<F>::MMAX - 1) {
     static const int r = knob(FTraits<F>::RB, RDefault<F>::RB);
     if (r == 8) return launch_block<F, M, 8>(fld, args, st);
@@ -115,6 +118,10 @@ static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t s
 
 template <class F, int K, bool INV>
 static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cudaStream_t st) {
+  if (args.io.mode != EMB_PLAIN) {  // application embeddings: one variant (R = 16)
+    if (INV && args.io.mode != EMB_POLY) return launch_cols<F, K, INV, 16>(fld, args, inst, st);
+    return launch_cols<F, K, INV, 16, true>(fld, args, inst, st);
+  }
   if constexpr (K >= 6 && K <= 10) {  // K = 11 with R = 8 would need 2048 threads
     static const int r = knob(FTraits<F>::RC, RDefault<F>::RC);
     if (r == 8) return launch_cols<F, K, INV, 8>(fld, args, inst, st);
@@ -142,7 +149,7 @@ static int dispatch_cols(int K, const F& fld, const ColArgs<F>& args, int64_t in
 
 template <class F>
 static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
-                      int64_t batch, cudaStream_t st, int dev) {
+                      int64_t batch, cudaStream_t st, int dev, const EmbedIO& io) {
   using E = typename F::T;
   using Tw = typename F::Tw;
   constexpr int MMAX = FTraits<F>::MMAX;
@@ -153,29 +160,34 @@ static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void
   else { lsi = dp.last_si64; lk = dp.last_k64; }
   const int64_t n = (int64_t)1 << L;
   if (L <= MMAX) {
-    BlockArgs<F> ba{(const E*)a, (const E*)b, (E*)c, batch, 0, twf, twi, lsi, lk};
+    BlockArgs<F> ba{(const E*)a, (const E*)b, (E*)c, batch, 0, twf, twi, lsi, lk, io};
     return dispatch_block<F>(L, fld, ba, st, std::make_integer_sequence<int, MMAX + 1>{});
   }
   const int K = L - MMAX;
   if (K > KMAX) return FCIRC_ESIZE;
+  const bool plain = io.mode == EMB_PLAIN;
   const int64_t per_inst = 2 * n * (int64_t)sizeof(E);
   int64_t C = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)chunk_bytes() / per_inst));
+  // plain: a' lives in c, b' in the workspace; embedded inputs: a' and b' both in the workspace
   void* ws;
-  int rc = get_workspace(dev, (void*)st, (size_t)(C * n) * sizeof(E), &ws);
+  int rc = get_workspace(dev, (void*)st, (size_t)((plain ? 1 : 2) * C * n) * sizeof(E), &ws);
   if (rc) return rc;
+  // instance strides of the caller's arrays (elements of E; 32-bit words for EMB_LIMBS)
+  const int64_t sa = plain ? n : io.na, sb = plain ? n : io.nb, sc = io.mode == EMB_POLY ? io.nc : n;
   for (int64_t i0 = 0; i0 < batch; i0 += C) {
     const int64_t cc = std::min<int64_t>(C, batch - i0);
-    const E* ai = (const E*)a + i0 * n;
-    const E* bi = (const E*)b + i0 * n;
-    E* ci = (E*)c + i0 * n;
-    E* bw = (E*)ws;
-    ColArgs<F> fa{ai, bi, ci, bw, n >> K, n, 0, 0, twf, twi, lsi, lk};
+    const E* ai = (const E*)a + i0 * sa;
+    const E* bi = (const E*)b + i0 * sb;
+    E* ci = (E*)c + i0 * sc;
+    E* ap = plain ? ci : (E*)ws;
+    E* bw = plain ? (E*)ws : (E*)ws + C * n;
+    ColArgs<F> fa{ai, bi, ap, bw, n >> K, n, 0, 0, twf, twi, lsi, lk, io};
     rc = dispatch_cols<F, false>(K, fld, fa, cc, st, std::make_integer_sequence<int, KMAX>{});
     if (rc) return rc;
-    BlockArgs<F> ba{ci, bw, ci, cc << K, K, twf, twi, lsi, lk};
+    BlockArgs<F> ba{ap, bw, ap, cc << K, K, twf, twi, lsi, lk, EmbedIO{}};
     rc = launch_block_r<F, MMAX>(fld, ba, st);
     if (rc) return rc;
-    ColArgs<F> ia{ci, nullptr, ci, nullptr, n >> K, n, 0, 0, twf, twi, lsi, lk};
+    ColArgs<F> ia{ap, nullptr, ci, nullptr, n >> K, n, 0, 0, twf, twi, lsi, lk, io};
     rc = dispatch_cols<F, true>(K, fld, ia, cc, st, std::make_integer_sequence<int, KMAX>{});
     if (rc) return rc;
   }

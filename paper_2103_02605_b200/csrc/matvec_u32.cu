@@ -4,8 +4,8 @@
 namespace fcirc {
 
 int run_matvec_u32(const FieldU32& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
-                   int64_t batch, cudaStream_t st, int dev) {
-  return run_matvec(fld, dp, a, b, c, L, batch, st, dev);
+                   int64_t batch, cudaStream_t st, int dev, const EmbedIO& io) {
+  return run_matvec(fld, dp, a, b, c, L, batch, st, dev, io);
 }
 
 }  // namespace fcirc

@@ -37,11 +37,13 @@ int knob(const char* name, int dflt);
 size_t chunk_bytes();
 
 // Per-field executors: all launches of one batched product on `st`.
-// a, b, c: [batch][2^L] device arrays of the field's element type; c may not alias a or b.
+// a, b, c: device arrays laid out as io describes; c may not alias a or b.
+// io: EMB_PLAIN for fcirc_matvec; the applications pass their embedding (fcirc_kernels.cuh EmbedIO).
+struct EmbedIO;
 int run_matvec_u32(const FieldU32& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
-                   int64_t batch, cudaStream_t st, int dev);
+                   int64_t batch, cudaStream_t st, int dev, const EmbedIO& io);
 int run_matvec_gold(const FieldGold& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
-                    int64_t batch, cudaStream_t st, int dev);
+                    int64_t batch, cudaStream_t st, int dev, const EmbedIO& io);
 
 // largest supported log2 n of the executors (multi-pass: MMAX + KMAX)
 int max_log_n(bool wide);

@@ -225,7 +225,10 @@ def test_nondefault_stream_and_repeatability():
 @pytest.mark.parametrize("p", [P998, GOLDILOCKS])
 def test_polymul_small_full(p):
     rng = np.random.default_rng(77)
-    for na, nb, batch in [(1, 1, 2), (2, 3, 2), (17, 33, 3), (1000, 24, 2), (4096, 4096, 2), (5000, 3000, 1)]:
+    # fused single pass (L <= 2^MMAX) and multi-pass (embedding fused into the first column pass,
+    # truncation into the last); degenerate one-coefficient operands on either side
+    for na, nb, batch in [(1, 1, 2), (2, 3, 2), (17, 33, 3), (1000, 24, 2), (4096, 4096, 2), (5000, 3000, 1),
+                          (1, 9000, 2), (9000, 1, 2), (10000, 7000, 2), (20000, 45000, 1)]:
         inp = synth.polymul_inputs(p, na, nb, batch, seed=int(rng.integers(1 << 30)))
         c = fc.polymul(_dev(inp["a"]), _dev(inp["b"]), p)
         c = _host(c)
@@ -269,7 +272,9 @@ def test_bigint_small():
 
 
 def test_bigint_edge_values():
-    for nx in [1, 2, 33]:
+    # all-ones operands: (2^32m - 1)^2 has a run of 0xFFFF digits, so the carry crosses many
+    # 2048-digit segments of the carry scan (nx = 5000: 20000 digits, 10 segments)
+    for nx in [1, 2, 33, 1025, 5000]:
         ones = np.full((1, nx), 0xFFFFFFFF, dtype=np.uint32)
         zeros = np.zeros((1, nx), dtype=np.uint32)
         one = np.zeros((1, nx), dtype=np.uint32)
