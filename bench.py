@@ -49,7 +49,6 @@ SM_MHZ = 1965.0
 MODMUL_PER_CLK_SM = {"u64": 8.0, "u32": 16.0}
 PRIMITIVE_MEASURED_PER_CLK_SM = {"u64": 3.16, "u32": 15.98}  # profiles/r01_peaks.jsonl (gold64 / shoup32)
 HBM_GBS_FALLBACK = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
-MMAX = {"u64": 12, "u32": 13}  # on-chip sub-problem size (matvec_impl.cuh FTraits::MMAX)
 
 WORKLOADS = {
     "C4_n20": "C4 @ n=2^20: Goldilocks f-circulant matvec, batch 64, f=w^n",
@@ -180,12 +179,11 @@ def whole_job_gelems(world: int, batch: int, n: int, steps: int, ms_max: float) 
     return world * batch * n * steps / (ms_max * 1e-3) / 1e9
 
 
-def algorithmic_modmuls(kind: str, n: int, batch: int, width: str) -> float:
+def algorithmic_modmuls(kind: str, n: int, batch: int, M: int, K: int) -> float:
     """Algorithmic modmuls per step attributed to one kernel kind:
-    M_const = 1.5 n L (0.5 n L each for the a split, the b split, the recombination), M_var = n."""
+    M_const = 1.5 n L (0.5 n L each for the a split, the b split, the recombination), M_var = n.
+    (M, K) = the library's pass schedule (fcirc_schedule): sub-problems of 2^M, K column levels."""
     L = n.bit_length() - 1
-    M = min(L, MMAX[width])
-    K = L - M
     if kind == "k_block_fused":
         return batch * n * (1.5 * L + 1)
     if kind == "k_block_sub":
@@ -423,7 +421,8 @@ def run_fcirc(args):
     width, n, batch = wl.width, wl.mm_n, wl.mm_batch
     dom = max((k for k in prof if prof[k][0] > 0), key=lambda k: prof[k][1])
     cnt, kms = prof[dom]
-    per_launch_mm = algorithmic_modmuls(dom, n, batch, width) * args.steps / cnt
+    sub_log, top = fc.schedule(wl.p, n)
+    per_launch_mm = algorithmic_modmuls(dom, n, batch, sub_log, top) * args.steps / cnt
     avg_ms = kms / cnt
     achieved = per_launch_mm / (avg_ms * 1e-3) / 1e12
     peak = SMS * SM_MHZ * 1e6 * MODMUL_PER_CLK_SM[width] / 1e12

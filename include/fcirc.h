@@ -115,6 +115,15 @@ const char* fcirc_strerror(int status);
 const char* fcirc_version(void);
 
 /*
+ * fcirc_schedule — HOST-only: the pass schedule fcirc_matvec uses for (p, n).
+ * *sub_log = log2 of the on-chip sub-problem size, *top_levels = number of recursion levels done by
+ * the column passes before / after the sub-problems (0: one fused pass over the whole product).
+ * Used by bench.py to attribute algorithmic work to kernels.
+ * Errors: FCIRC_EINVAL (null output, n not a power of two), FCIRC_EPRIME, FCIRC_ESIZE.
+ */
+int fcirc_schedule(uint64_t p, int64_t n, int* sub_log, int* top_levels);
+
+/*
  * fcirc_last_launch_count — number of kernels the calling host thread launched in its most
  * recent successful libfcirc call (for the benchmark's gpu_launches count).
  */

@@ -19,7 +19,7 @@ import os
 import numpy as np
 
 __all__ = ["FcircError", "matvec", "matvec_host", "polymul", "bigint_mul", "plan_table", "strerror",
-           "last_launch_count", "release_cache", "version", "library_path", "P998", "P469", "P167",
+           "last_launch_count", "release_cache", "version", "library_path", "schedule", "P998", "P469", "P167",
            "GOLDILOCKS", "PRIMES"]
 
 P998 = 998244353
@@ -57,9 +57,11 @@ def _load():
     lib.fcirc_polymul.argtypes = [u64, vp, i64, vp, i64, vp, i64, vp]
     lib.bigint_mul.argtypes = [vp, i64, vp, i64, vp, i64, vp]
     lib.fcirc_plan_table.argtypes = [u64, u64, i64, vp, vp, ctypes.POINTER(u64), ctypes.POINTER(u64)]
+    lib.fcirc_schedule.argtypes = [u64, i64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
     lib.fcirc_profile_enable.argtypes = [ctypes.c_int]
     lib.fcirc_profile_read.argtypes = [vp, vp, ctypes.c_int]
     for fn in (lib.fcirc_matvec, lib.fcirc_matvec_host, lib.fcirc_polymul, lib.bigint_mul, lib.fcirc_plan_table,
+               lib.fcirc_schedule,
                lib.fcirc_release_cache, lib.fcirc_profile_enable, lib.fcirc_profile_read):
         fn.restype = ctypes.c_int
     lib.fcirc_strerror.argtypes = [ctypes.c_int]
@@ -220,6 +222,15 @@ def bigint_mul(x, y, out=None, stream=None):
     rc = _load().bigint_mul(x.data_ptr(), nx, y.data_ptr(), ny, out.data_ptr(), batch, _stream_handle(stream))
     _check(rc, "bigint_mul")
     return out
+
+
+def schedule(p: int, n: int):
+    """Host-only: (log2 of the on-chip sub-problem size, number of column-pass levels) that
+    fcirc_matvec uses for (p, n) (fcirc_schedule)."""
+    m = ctypes.c_int(0)
+    k = ctypes.c_int(0)
+    _check(_load().fcirc_schedule(int(p), int(n), ctypes.byref(m), ctypes.byref(k)), "fcirc_schedule")
+    return int(m.value), int(k.value)
 
 
 def plan_table(p: int, f: int, n: int):

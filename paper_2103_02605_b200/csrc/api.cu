@@ -433,6 +433,19 @@ int fcirc_plan_table(uint64_t p, uint64_t f, int64_t n, uint64_t* s, uint64_t* s
 
 const char* fcirc_version(void) { return "libfcirc 0.1 sm_100a"; }
 
+int fcirc_schedule(uint64_t p, int64_t n, int* sub_log, int* top_levels) {
+  if (!sub_log || !top_levels) return FCIRC_EINVAL;
+  const int L = ilog2_exact(n);
+  if (L < 0) return FCIRC_EINVAL;
+  const PrimeInfo* pi = prime_info(p);
+  if (!pi) return FCIRC_EPRIME;
+  if (L > pi->two_adicity || L > max_log_n(pi->wide)) return FCIRC_ESIZE;
+  const int S = split_log_n(pi->wide, L);
+  *sub_log = L <= S ? L : S;
+  *top_levels = L <= S ? 0 : L - S;
+  return FCIRC_OK;
+}
+
 int64_t fcirc_last_launch_count(void) { return g_launches; }
 
 int fcirc_profile_enable(int on) {

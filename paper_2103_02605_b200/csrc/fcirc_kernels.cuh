@@ -129,7 +129,14 @@ struct BlockArgs {
   EmbedIO io;               // k == 0 and EMB only: embedding of the loads / truncation of the stores
 };
 
-template <class F, int M, int R, int IPC, int MINB = 1, bool EMB = false>
+// k_block stages its twiddle slices in shared memory for the 32-bit fields (see TWS below), at
+// swizzled positions i ^ ((i >> 4) & 31) (a bijection of [0, 2^M)): the model in
+// tools/bank_model.py gives 1.2x the conflict-free wavefronts instead of 1.5x unswizzled
+__device__ __forceinline__ int tw_swz(int i) { return i ^ ((i >> 4) & 31); }
+template <class F, int M> struct TwStage { static constexpr bool value = false; };
+template <int M> struct TwStage<FieldU32, M> { static constexpr bool value = M >= 6; };
+
+template <class F, int M, int R, int IPC, int MINB = 1, bool EMB = false, bool TWS = false>
 __global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
 k_block(F fld, BlockArgs<F> args) {
   using T = typename F::T;
@@ -154,6 +161,33 @@ k_block(F fld, BlockArgs<F> args) {
   const int64_t inst = (int64_t)(blockIdx.x >> k) * IPC + li;
   const bool active = inst < batch;
   const int64_t base = ((inst << k) + E) * m;
+
+  // Twiddle staging (32-bit fields): the CTA's sub-block uses the heap slice
+  // {2^(k+j) + E 2^j + e' : j < M, e' < 2^j} of each table (contiguous per level).
+  // It is copied once, coalesced, into shared memory at local heap index 2^j - 1 + e', so the
+  // butterflies read twiddles with LDS instead of scattered L2 loads (profiles/r01c: the u32
+  // k_block stalled on long_scoreboard).  Goldilocks is arithmetic-bound and keeps the LDG path;
+  // so does the fused whole-product launch (k = 0), whose CTAs all share one table via L1/L2.
+  Tw* twsf = reinterpret_cast<Tw*>(sm + (size_t)IPC * 2 * PM);
+  Tw* twsi = twsf + m;
+  if constexpr (TWS) {
+    for (int q = threadIdx.x; q < m - 1; q += blockDim.x) {
+      const int j = 31 - __clz(q + 1);
+      const int e = q + 1 - (1 << j);
+      const int g = (1 << (k + j)) + (E << j) + e;
+      twsf[tw_swz(q)] = args.twf[g];
+      twsi[tw_swz(q)] = args.twi[g];
+    }
+    __syncthreads();
+  }
+  auto twf_at = [&](int ph_bbit, int xaddr) -> Tw {   // forward twiddle of pair bit b at address x
+    if constexpr (TWS) return twsf[tw_swz((1 << (M - 1 - ph_bbit)) - 1 + (xaddr >> (ph_bbit + 1)))];
+    else return args.twf[(gbase | xaddr) >> (ph_bbit + 1)];
+  };
+  auto twi_at = [&](int ph_bbit, int xaddr) -> Tw {
+    if constexpr (TWS) return twsi[tw_swz((1 << (M - 1 - ph_bbit)) - 1 + (xaddr >> (ph_bbit + 1)))];
+    else return args.twi[(gbase | xaddr) >> (ph_bbit + 1)];
+  };
 
   T xa[R], xb[R];
   // ---- load (phase-0 addresses: slot s at s * 2^lo + t, coalesced across t)
@@ -198,17 +232,16 @@ k_block(F fld, BlockArgs<F> args) {
       __syncthreads();
     }
     const int rp = PH::rp(ph), lo = PH::lo(ph);
-    const int tb = gbase | PH::ins_t(ph, t);
+    const int tb = PH::ins_t(ph, t);
 #pragma unroll
     for (int l = 0; l < rp; ++l) {
       const int jb = rp - 1 - l;
       const int bbit = lo + jb;
-      const int tsh = tb >> (bbit + 1);
 #pragma unroll
       for (int s0 = 0; s0 < R; ++s0) {
         if ((s0 >> jb) & 1) continue;
         const int s1 = s0 + (1 << jb);
-        const Tw tw = args.twf[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+        const Tw tw = twf_at(bbit, tb | PH::cslot(ph, s0));
         fld.fwd_a(xa[s0], xa[s1], tw);
         fld.fwd_b(xb[s0], xb[s1], tw);
       }
@@ -242,12 +275,11 @@ k_block(F fld, BlockArgs<F> args) {
       __syncthreads();
     }
     const int rp = PH::rp(ph), lo = PH::lo(ph);
-    const int tb = gbase | PH::ins_t(ph, t);
+    const int tb = PH::ins_t(ph, t);
 #pragma unroll
     for (int l = 0; l < rp; ++l) {
       const int jb = l;
       const int bbit = lo + jb;
-      const int tsh = tb >> (bbit + 1);
 #pragma unroll
       for (int s0 = 0; s0 < R; ++s0) {
         if ((s0 >> jb) & 1) continue;
@@ -255,7 +287,7 @@ k_block(F fld, BlockArgs<F> args) {
         if (bbit == M - 1 && top) {
           fld.inv_last(xm[s0], xm[s1], args.last_si, args.last_k);
         } else {
-          const Tw tw = args.twi[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+          const Tw tw = twi_at(bbit, tb | PH::cslot(ph, s0));
           fld.inv(xm[s0], xm[s1], tw);
         }
       }

@@ -9,5 +9,6 @@ int run_matvec_gold(const FieldGold& fld, const DevPlan& dp, const void* a, cons
 }
 
 int max_log_n(bool wide) { return (wide ? FTraits<FieldGold>::MMAX : FTraits<FieldU32>::MMAX) + KMAX; }
+int split_log_n(bool wide, int L) { return wide ? msplit<FieldGold>(L) : split_log_n_u32(L); }
 
 }  // namespace fcirc

@@ -19,14 +19,18 @@ namespace fcirc {
 
 template <class F> struct FTraits;
 template <> struct FTraits<FieldU32> {
-  static constexpr int MMAX = 13;   // 2 x 2^13 x 4 B + pad = 66 KB smem per sub-problem
+  static constexpr int MMAX = 13;   // 2 x 2^13 x 4 B data + 2 x 2^13 x 8 B staged twiddles = 192 KB smem
+  static constexpr int MPREF = 12;  // 96 KB: two CTAs per SM
   static constexpr const char* RB = "U32_RB";
   static constexpr const char* RC = "U32_RC";
+  static constexpr const char* MS = "U32_MSPLIT";
 };
 template <> struct FTraits<FieldGold> {
-  static constexpr int MMAX = 12;   // 2 x 2^12 x 8 B + pad = 70 KB smem per sub-problem
+  static constexpr int MMAX = 12;   // 2 x 2^12 x 8 B = 64 KB smem per sub-problem
+  static constexpr int MPREF = 12;
   static constexpr const char* RB = "GOLD_RB";
   static constexpr const char* RC = "GOLD_RC";
+  static constexpr const char* MS = "GOLD_MSPLIT";
 };
 constexpr int KMAX = 11;
 
@@ -40,17 +44,17 @@ template <int RR> constexpr int wsel(int K) {
   return (256 * rsel<RR>(K)) >> K < 8 ? 8 : ((256 * rsel<RR>(K)) >> K);
 }
 
-template <class F, int M, int RR, bool EMB = false>
-static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
+template <class F, int M, int RR, bool EMB, bool TWS>
+static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
   constexpr int R = rsel<RR>(M), IPC = ipcsel<RR>(M);
   constexpr int T = (1 << M) / R;
   using E = typename F::T;
   constexpr int PM = 1 << M;  // swizzled, unpadded (fcirc_kernels.cuh swz)
-  const size_t smem = (size_t)IPC * 2 * PM * sizeof(E);
+  const size_t smem = (size_t)IPC * 2 * PM * sizeof(E) + (TWS ? (size_t)2 * (1 << M) * sizeof(typename F::Tw) : 0);
   // occupancy target: 1024 resident threads per SM for R <= 8 (register cap 64), 512 for R = 16
   // (cap 128: without a floor ptxas spends ~190 registers and halves the resident warps)
   constexpr int MINB = (T * IPC < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / (T * IPC) : 1;
-  auto kern = k_block<F, M, R, IPC, MINB, EMB>;
+  auto kern = k_block<F, M, R, IPC, MINB, EMB, TWS>;
   if (smem > 48 * 1024) {
     static bool once = false;  // attribute set per kernel instantiation
     if (!once) {
@@ -66,6 +70,14 @@ static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st)
   prof_end(st);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+// sub-problem launches (k > 0) of the 32-bit fields stage their twiddle slices in smem
+template <class F, int M, int RR, bool EMB = false>
+static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
+  if constexpr (TwStage<F, M>::value && !EMB)
+    if (args.k > 0) return launch_block_t<F, M, RR, false, true>(fld, args, st);
+  return launch_block_t<F, M, RR, EMB, false>(fld, args, st);
 }
 
 template <class F, int K, bool INV, int RR, bool EMB = false>
@@ -147,12 +159,22 @@ static int dispatch_cols(int K, const F& fld, const ColArgs<F>& args, int64_t in
   return rc;
 }
 
+// On-chip sub-problem size for a product of order 2^L: the preferred split (FCIRC_<field>_MSPLIT,
+// default FTraits::MPREF; u32 prefers 2^12 = two CTAs per SM over 2^13 = one, profiles/r01d), grown
+// up to MMAX only when the column passes would need more than KMAX levels.
+template <class F>
+static int msplit(int L) {
+  static const int pref = std::min(FTraits<F>::MMAX,
+                                   std::max(FTraits<F>::MMAX - 1, knob(FTraits<F>::MS, FTraits<F>::MPREF)));
+  return std::min(FTraits<F>::MMAX, std::max(pref, L - KMAX));
+}
+
 template <class F>
 static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
                       int64_t batch, cudaStream_t st, int dev, const EmbedIO& io) {
   using E = typename F::T;
   using Tw = typename F::Tw;
-  constexpr int MMAX = FTraits<F>::MMAX;
+  const int MMAX = msplit<F>(L);
   const Tw* twf = (const Tw*)dp.twf;
   const Tw* twi = (const Tw*)dp.twi;
   Tw lsi, lk;
@@ -161,7 +183,7 @@ static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void
   const int64_t n = (int64_t)1 << L;
   if (L <= MMAX) {
     BlockArgs<F> ba{(const E*)a, (const E*)b, (E*)c, batch, 0, twf, twi, lsi, lk, io};
-    return dispatch_block<F>(L, fld, ba, st, std::make_integer_sequence<int, MMAX + 1>{});
+    return dispatch_block<F>(L, fld, ba, st, std::make_integer_sequence<int, FTraits<F>::MMAX + 1>{});
   }
   const int K = L - MMAX;
   if (K > KMAX) return FCIRC_ESIZE;
@@ -185,7 +207,7 @@ static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void
     rc = dispatch_cols<F, false>(K, fld, fa, cc, st, std::make_integer_sequence<int, KMAX>{});
     if (rc) return rc;
     BlockArgs<F> ba{ap, bw, ap, cc << K, K, twf, twi, lsi, lk, EmbedIO{}};
-    rc = launch_block_r<F, MMAX>(fld, ba, st);
+    rc = dispatch_block<F>(MMAX, fld, ba, st, std::make_integer_sequence<int, FTraits<F>::MMAX + 1>{});
     if (rc) return rc;
     ColArgs<F> ia{ap, nullptr, ci, nullptr, n >> K, n, 0, 0, twf, twi, lsi, lk, io};
     rc = dispatch_cols<F, true>(K, fld, ia, cc, st, std::make_integer_sequence<int, KMAX>{});

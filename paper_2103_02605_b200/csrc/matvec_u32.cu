@@ -8,4 +8,6 @@ int run_matvec_u32(const FieldU32& fld, const DevPlan& dp, const void* a, const 
   return run_matvec(fld, dp, a, b, c, L, batch, st, dev, io);
 }
 
+int split_log_n_u32(int L) { return msplit<FieldU32>(L); }
+
 }  // namespace fcirc

@@ -45,7 +45,10 @@ int run_matvec_u32(const FieldU32& fld, const DevPlan& dp, const void* a, const 
 int run_matvec_gold(const FieldGold& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
                     int64_t batch, cudaStream_t st, int dev, const EmbedIO& io);
 
-// largest supported log2 n of the executors (multi-pass: MMAX + KMAX)
+// largest supported log2 n of the executors (multi-pass: sub-problem size + KMAX)
 int max_log_n(bool wide);
+// log2 of the on-chip sub-problem size for n = 2^L (L <= split: one fused pass; else sub-problems)
+int split_log_n(bool wide, int L);
+int split_log_n_u32(int L);
 
 }  // namespace fcirc

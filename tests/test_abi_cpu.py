@@ -156,3 +156,19 @@ def test_product_package_does_not_touch_oracle():
         if os.path.isfile(path) and path.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
             text = open(path).read()
             assert "import oracle" not in text and "from oracle" not in text and "liboracle" not in text, path
+
+
+def test_schedule_host_only():
+    """fcirc_schedule: one fused pass up to the on-chip size, then sub-problems + column levels."""
+    for p in PRIMES:
+        m_fused, k0 = fc.schedule(p, 1 << 10)
+        assert (m_fused, k0) == (10, 0)
+        M, K = fc.schedule(p, 1 << 20)
+        assert M + K == 20 and 11 <= M <= 13 and K >= 7
+    # the sub-problem grows only when the column passes would exceed 11 levels
+    M, K = fc.schedule(P469, 1 << 24)
+    assert (M, K) == (13, 11)
+    with pytest.raises(fc.FcircError):
+        fc.schedule(P998, 12)
+    with pytest.raises(fc.FcircError):
+        fc.schedule(12345, 16)

@@ -85,6 +85,25 @@ def ratio_cols(K, R, W, esz, rowmap, short_first):
     return tot / ideal
 
 
+def ratio_twiddles(M, R, swz):
+    """k_block with staged twiddles: LDS.64 of the twiddle of each butterfly (local heap index)."""
+    P = Phases(M, R, True)
+    tot = ideal = 0
+    for ph in range(P.NPH):
+        rp, lo = P.rp(ph), P.lo(ph)
+        for l in range(rp):
+            bbit = lo + rp - 1 - l
+            for s0 in range(R):
+                if (s0 >> (rp - 1 - l)) & 1:
+                    continue
+                for w0 in range(0, P.T, 32):
+                    ad = sorted({swz((1 << (M - 1 - bbit)) - 1 + ((P.ins_t(ph, t) | P.cslot(ph, s0)) >> (bbit + 1)))
+                                 for t in range(w0, min(w0 + 32, P.T))})
+                    tot += wavefronts(ad, 8) if len(ad) > 1 else 1
+                    ideal += 1 if len(ad) <= 16 else 2
+    return tot / ideal
+
+
 def main():
     for esz, sh, mask in [(4, 5, 31), (8, 4, 15)]:
         for R in (4, 8, 16):
@@ -110,6 +129,10 @@ def main():
                 new = ratio_cols(K, R, W, esz, lambda x: x ^ ((x >> r) & 7), True)
                 cells.append(f"K{K}/W{W}:{old:.2f}/{new:.2f}")
             print(f"{esz}B R={R:2d} " + " ".join(cells))
+    print("k_block staged twiddles (8 B): plain index / i ^ ((i >> 4) & 31)")
+    for M, R in [(11, 8), (12, 8), (13, 8), (12, 16)]:
+        print(f"M{M} R={R}: {ratio_twiddles(M, R, lambda i: i):.2f} / "
+              f"{ratio_twiddles(M, R, lambda i: i ^ ((i >> 4) & 31)):.2f}")
 
 
 if __name__ == "__main__":
