@@ -19,7 +19,10 @@
 //             1/n scaling and canonicalisation (K5).  Same register/shared-memory phase scheme
 //             along the column; W consecutive columns per CTA for coalescing.
 #pragma once
+#include <cuda.h>
+
 #include <cstdint>
+
 #include "modarith.cuh"
 
 namespace fcirc {
@@ -440,6 +443,190 @@ k_cols(F fld, ColArgs<F> args) {
 #pragma unroll
       for (int s = 0; s < R; ++s) io_store(dst, inst, col + (int64_t)(rb + PH::cslot(0, s)) * m, args.n, x[s], args.io);
     }
+  }
+}
+
+
+// ------------------------------------------------------------------------------------------
+// k_cols_tma: persistent, TMA-pipelined version of k_cols for plain [batch][n] operands.
+//
+// Each CTA loops over column tiles (W consecutive columns x all 2^K rows of one instance, one of
+// a or b in the forward pass).  One elected thread issues the Tensor Memory Accelerator copy
+// (cp.async.bulk.tensor, 3-D map {column, row, instance}) of tile i+1 into the second of two
+// shared-memory stages while the CTA transforms tile i, completion signalled through an mbarrier
+// with the tile's byte count -- the HBM/L2 latency of the strided column reads is hidden behind
+// the integer work instead of stalling each CTA at its start (profiles/r01d: long_scoreboard
+// was the top stall of the column passes).  The butterflies, phase exchanges (swizzled smem) and
+// stores are those of k_cols.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kTmaBoxRows = 256;   // TMA box extent limit per dimension
+
+template <class F, int K, int R, int W, bool INV, int MINB = 1>
+__global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
+k_cols_tma(F fld, ColArgs<F> args, const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
+           int64_t ntiles) {
+  using T = typename F::T;
+  using Tw = typename F::Tw;
+  using PH = Phases<K, R>;
+  constexpr int NPH = PH::NPH;
+  constexpr int ROWS = 1 << K;
+  constexpr uint32_t TILE_BYTES = (uint32_t)(ROWS * W * sizeof(T));
+  // dynamic smem only (a static __shared__ variable would shift the dynamic base off the 128-byte
+  // alignment TMA destinations need): [stage 0][stage 1][exchange][2 mbarriers]
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // round the base up to 128 bytes in the shared window (the launch adds 128 bytes of slack)
+  const uint32_t raw = smem_u32(smem_raw);
+  T* stage_buf = reinterpret_cast<T*>(smem_raw + (((raw + 127u) & ~127u) - raw));  // 2 x [ROWS][W] dense
+  T* sm = stage_buf + 2 * ROWS * W;                          // exchange buffer, swizzled rows
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + ROWS * W);
+
+  const int c = threadIdx.x % W;
+  const int t = threadIdx.x / W;
+  const int64_t m = args.m;
+  auto sidx = [&](int row) { return (row ^ ((row >> PH::r) & 7)) * W + c; };
+
+  // tile -> (instance, column block, operand): forward tiles alternate a / b
+  auto decode = [&](int64_t tile, int64_t& inst, int64_t& cb, int& second) {
+    const int64_t unit = INV ? tile : (tile >> 1);
+    second = INV ? 0 : (int)(tile & 1);
+    inst = unit / args.colblocks;
+    cb = unit - inst * args.colblocks;
+  };
+  auto issue = [&](int64_t tile, int st) {
+    int64_t inst, cb;
+    int second;
+    decode(tile, inst, cb, second);
+    const CUtensorMap* map = second ? &map1 : &map0;
+    mbar_expect_tx(&bars[st], TILE_BYTES);
+#pragma unroll
+    for (int rb = 0; rb < ROWS; rb += kTmaBoxRows)
+      tma_load_3d(stage_buf + (size_t)st * ROWS * W + (size_t)rb * W, map, (int)(cb * W), rb, (int)inst, &bars[st]);
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int64_t tile = blockIdx.x;
+  if (threadIdx.x == 0 && tile < ntiles) issue(tile, 0);
+
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int st = it & 1;
+    if (threadIdx.x == 0 && tile + gridDim.x < ntiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of that stage done
+      issue(tile + gridDim.x, st ^ 1);
+    }
+    int64_t inst, cb;
+    int second;
+    decode(tile, inst, cb, second);
+    const int64_t base = inst * args.n + cb * W + c;
+    T* dst = second ? args.dst1 : args.dst0;
+    mbar_wait(&bars[st], (uint32_t)((it >> 1) & 1));
+    const T* tb_s = stage_buf + (size_t)st * ROWS * W;
+
+    T x[R];
+    const int ph_first = INV ? NPH - 1 : 0;
+    {
+      const int rb = PH::ins_t(ph_first, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) x[s] = tb_s[(rb + PH::cslot(ph_first, s)) * W + c];
+    }
+    if (!INV) {
+#pragma unroll
+      for (int ph = 0; ph < NPH; ++ph) {
+        if (ph > 0) {
+          const int wb = PH::ins_t(ph - 1, t);
+#pragma unroll
+          for (int s = 0; s < R; ++s) sm[sidx(wb + PH::cslot(ph - 1, s))] = x[s];
+          __syncthreads();
+          const int rb = PH::ins_t(ph, t);
+#pragma unroll
+          for (int s = 0; s < R; ++s) x[s] = sm[sidx(rb + PH::cslot(ph, s))];
+          __syncthreads();
+        }
+        const int rp = PH::rp(ph), lo = PH::lo(ph);
+        const int tb = (1 << K) | PH::ins_t(ph, t);
+#pragma unroll
+        for (int l = 0; l < rp; ++l) {
+          const int jb = rp - 1 - l;
+          const int bbit = lo + jb;
+          const int tsh = tb >> (bbit + 1);
+#pragma unroll
+          for (int s0 = 0; s0 < R; ++s0) {
+            if ((s0 >> jb) & 1) continue;
+            const int s1 = s0 + (1 << jb);
+            const Tw tw = args.twf[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+            if (second) fld.fwd_b(x[s0], x[s1], tw);
+            else fld.fwd_a(x[s0], x[s1], tw);
+          }
+        }
+      }
+      const int rb = PH::ins_t(NPH - 1, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(NPH - 1, s)) * m] = x[s];
+    } else {
+#pragma unroll
+      for (int ph = NPH - 1; ph >= 0; --ph) {
+        if (ph < NPH - 1) {
+          const int wb = PH::ins_t(ph + 1, t);
+#pragma unroll
+          for (int s = 0; s < R; ++s) sm[sidx(wb + PH::cslot(ph + 1, s))] = x[s];
+          __syncthreads();
+          const int rb = PH::ins_t(ph, t);
+#pragma unroll
+          for (int s = 0; s < R; ++s) x[s] = sm[sidx(rb + PH::cslot(ph, s))];
+          __syncthreads();
+        }
+        const int rp = PH::rp(ph), lo = PH::lo(ph);
+        const int tb = (1 << K) | PH::ins_t(ph, t);
+#pragma unroll
+        for (int l = 0; l < rp; ++l) {
+          const int jb = l;
+          const int bbit = lo + jb;
+          const int tsh = tb >> (bbit + 1);
+#pragma unroll
+          for (int s0 = 0; s0 < R; ++s0) {
+            if ((s0 >> jb) & 1) continue;
+            const int s1 = s0 + (1 << jb);
+            if (bbit == K - 1) {
+              fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
+            } else {
+              const Tw tw = args.twi[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+              fld.inv(x[s0], x[s1], tw);
+            }
+          }
+        }
+      }
+      const int rb = PH::ins_t(0, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(0, s)) * m] = x[s];
+    }
+    __syncthreads();   // stage st and the exchange buffer are free for the next issue / tile
   }
 }
 

@@ -11,6 +11,8 @@
 #include <cstdint>
 #include <utility>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/fcirc.h"
 #include "fcirc_kernels.cuh"
 #include "runtime.h"
@@ -26,8 +28,8 @@ template <> struct FTraits<FieldU32> {
   static constexpr const char* MS = "U32_MSPLIT";
 };
 template <> struct FTraits<FieldGold> {
-  static constexpr int MMAX = 12;   // 2 x 2^12 x 8 B = 64 KB smem per sub-problem
-  static constexpr int MPREF = 12;
+  static constexpr int MMAX = 13;   // 2 x 2^13 x 8 B = 128 KB smem per sub-problem
+  static constexpr int MPREF = 12;  // 64 KB: two CTAs per SM
   static constexpr const char* RB = "GOLD_RB";
   static constexpr const char* RC = "GOLD_RC";
   static constexpr const char* MS = "GOLD_MSPLIT";
@@ -106,6 +108,71 @@ static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStr
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
 
+// ---- TMA-pipelined column passes (k_cols_tma): tensor maps through the driver entry point
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }();
+  return fn;
+}
+
+// 3-D view {column < m, row < 2^K, instance} of a [instances][n] array, box {W, min(2^K, 256), 1}
+template <class E>
+static bool make_col_map(CUtensorMap* map, const void* base, int64_t m, int K, int64_t instances, int W) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)m, (cuuint64_t)1 << K, (cuuint64_t)instances};
+  const cuuint64_t strides[2] = {(cuuint64_t)m * sizeof(E), ((cuuint64_t)m << K) * sizeof(E)};
+  const cuuint32_t box[3] = {(cuuint32_t)W, (cuuint32_t)std::min(1 << K, kTmaBoxRows), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, sizeof(E) == 8 ? CU_TENSOR_MAP_DATA_TYPE_UINT64 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 3,
+             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class F, int K, bool INV, int RR>
+static int launch_cols_tma(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
+  constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
+  constexpr int threads = W * ((1 << K) / R);
+  using E = typename F::T;
+  // two TMA stages + exchange buffer + 2 mbarriers + 128 bytes of alignment slack
+  const size_t smem = (size_t)3 * (1 << K) * W * sizeof(E) + 16 + 128;
+  constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
+  auto kern = k_cols_tma<F, K, R, W, INV, MINB>;
+  static int occ = -1;   // resident CTAs per SM (per instantiation)
+  if (occ < 0) {
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return FCIRC_ECUDA;
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem) != cudaSuccess || o < 1)
+      return FCIRC_ECUDA;
+    occ = o;
+  }
+  args.colblocks = args.m / W;
+  args.units = instances * args.colblocks;
+  CUtensorMap m0, m1;
+  if (!make_col_map<E>(&m0, args.src0, args.m, K, instances, W)) return FCIRC_ECUDA;
+  if (!INV && !make_col_map<E>(&m1, args.src1, args.m, K, instances, W)) return FCIRC_ECUDA;
+  if (INV) m1 = m0;
+  const int64_t ntiles = args.units * (INV ? 1 : 2);
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * occ);
+  prof_begin(INV ? 3 : 2, st);
+  kern<<<(unsigned)grid, threads, smem, st>>>(fld, args, m0, m1, ntiles);
+  prof_end(st);
+  count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
 // Register-blocking variants: the two largest sub-problem sizes and the deep column
 // transforms are instantiated with R = 16, 8 and 4 elements per thread, selected by the runtime
 // knobs FCIRC_<field>_RB / _RC (defaults from the measured sweep, profiles/r01c_sweep.txt).
@@ -133,6 +200,17 @@ static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cud
   if (args.io.mode != EMB_PLAIN) {  // application embeddings: one variant (R = 16)
     if (INV && args.io.mode != EMB_POLY) return launch_cols<F, K, INV, 16>(fld, args, inst, st);
     return launch_cols<F, K, INV, 16, true>(fld, args, inst, st);
+  }
+  static const int use_tma = knob("TMA", 1);
+  using E = typename F::T;
+  // TMA pipeline when two stages + the exchange buffer fit in shared memory
+  if constexpr (K >= 5 && 3 * (1 << K) * wsel<16>(K) * sizeof(E) <= 200 * 1024) {
+    if (use_tma) {
+      static const int r = knob(FTraits<F>::RC, RDefault<F>::RC);
+      if constexpr (K <= 10)
+        if (r == 8) return launch_cols_tma<F, K, INV, 8>(fld, args, inst, st);
+      return launch_cols_tma<F, K, INV, 16>(fld, args, inst, st);
+    }
   }
   if constexpr (K >= 6 && K <= 10) {  // K = 11 with R = 8 would need 2048 threads
     static const int r = knob(FTraits<F>::RC, RDefault<F>::RC);

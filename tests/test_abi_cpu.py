@@ -56,7 +56,7 @@ def test_argument_validation_before_device():
     assert _call_matvec(P998, 1, 16, 4, a=3, c=3) == -1  # c overlaps a
     assert _call_matvec(1000003, 1, 16, 1) == -2         # p not in the registry
     assert _call_matvec(P998, 1, 1 << 24, 1) == -4       # 2^24 does not divide p-1
-    assert _call_matvec(GOLDILOCKS, 1, 1 << 24, 1) == -4  # above the maximum (2^(MMAX+KMAX) = 2^23)
+    assert _call_matvec(GOLDILOCKS, 1, 1 << 25, 1) == -4  # above the maximum (2^(MMAX+KMAX) = 2^24)
     assert _call_matvec(P469, 1, 1 << 25, 1) == -4        # 2^25 | p-1 but above the 32-bit maximum 2^24
     assert _call_matvec(P998, 0, 16, 1) == -3            # f = 0: no f^-1
     assert _call_matvec(P998, P998, 16, 1) == -3         # f == 0 mod p

@@ -119,7 +119,7 @@ def test_matvec_extreme_values():
 def test_matvec_multipass_sampled(p):
     """n = 2^13 .. the maximum (2^23, or 2^24 for the primes with 2-adicity > 23): three-pass
     schedule, sampled entries + checksum."""
-    top = {P998: 23, P469: 24, P167: 24, GOLDILOCKS: 23}[p]
+    top = {P998: 23, P469: 24, P167: 24, GOLDILOCKS: 24}[p]
     for L in range(13, top + 1):
         batch = 3 if L <= 18 else 1
         inp = synth.matvec_inputs(p, 1 << L, batch, seed=200 + L)
