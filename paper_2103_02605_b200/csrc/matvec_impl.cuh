@@ -26,6 +26,7 @@ template <> struct FTraits<FieldU32> {
   static constexpr const char* RB = "U32_RB";
   static constexpr const char* RC = "U32_RC";
   static constexpr const char* MS = "U32_MSPLIT";
+  static constexpr int TMA_MIN_K = 5;   // TMA column passes from this depth on (profiles/r01e)
 };
 template <> struct FTraits<FieldGold> {
   static constexpr int MMAX = 13;   // 2 x 2^13 x 8 B = 128 KB smem per sub-problem
@@ -33,6 +34,7 @@ template <> struct FTraits<FieldGold> {
   static constexpr const char* RB = "GOLD_RB";
   static constexpr const char* RC = "GOLD_RC";
   static constexpr const char* MS = "GOLD_MSPLIT";
+  static constexpr int TMA_MIN_K = 9;   // at K = 8 the TMA pipeline measured 2 % slower than k_cols
 };
 constexpr int KMAX = 11;
 
@@ -204,7 +206,7 @@ static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cud
   static const int use_tma = knob("TMA", 1);
   using E = typename F::T;
   // TMA pipeline when two stages + the exchange buffer fit in shared memory
-  if constexpr (K >= 5 && 3 * (1 << K) * wsel<16>(K) * sizeof(E) <= 200 * 1024) {
+  if constexpr (K >= FTraits<F>::TMA_MIN_K && 3 * (1 << K) * wsel<16>(K) * sizeof(E) <= 200 * 1024) {
     if (use_tma) {
       static const int r = knob(FTraits<F>::RC, RDefault<F>::RC);
       if constexpr (K <= 10)

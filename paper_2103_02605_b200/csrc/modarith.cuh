@@ -117,7 +117,7 @@ struct FieldGold {
 
   // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS;
   // a + b - 2^64 + EPS <= (2^64-1) + (p-1) - 2^64 + EPS = 2^64 - 2: no second carry.  Weak result.
-  __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
+  __device__ __forceinline__ static uint64_t add_c_m(uint64_t a, uint64_t b) {
     uint32_t s0, s1;
     asm("{\n\t.reg .u32 m;\n\t"
         "add.cc.u32  %0, %2, %4;\n\t"
@@ -127,6 +127,22 @@ struct FieldGold {
         "addc.u32    %1, %1, 0;\n\t"
         "}"
         : "=&r"(s0), "=&r"(s1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(s0, s1);
+  }
+  // The same sum with the correction as selects (ALU pipe) instead of a mask multiply-add (FMA
+  // pipe): + EPS = (lo - 1) with a carry into hi unless lo == 0.  Used by the forward butterflies,
+  // where it balances the pipes (+8-10 % butterflies/clk, profiles/r01e_gold_butterfly_*.jsonl);
+  // the inverse butterflies keep add_c_m (faster there).
+  __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
+    uint32_t s0, s1, c;
+    asm("add.cc.u32  %0, %3, %5;\n\t"
+        "addc.cc.u32 %1, %4, %6;\n\t"
+        "addc.u32    %2, 0, 0;"
+        : "=r"(s0), "=r"(s1), "=r"(c) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    if (c) {
+      s1 = s0 == 0u ? s1 : s1 + 1u;
+      s0 = s0 - 1u;
+    }
     return mk(s0, s1);
   }
   // a - b mod p for a any 64-bit value and b < p: on a borrow subtract EPS; the wrapped value is
@@ -166,7 +182,7 @@ struct FieldGold {
   //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
   //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
   //   canonicalise: u = r + EPS carries iff r >= p; then r += EPS * carry (mod 2^64) = r - p.
-  __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+  __device__ __forceinline__ static uint64_t reduce4_m(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
     uint32_t r0, r1;
     asm("{\n\t.reg .u32 c, m, h;\n\t"
         "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
@@ -188,11 +204,35 @@ struct FieldGold {
         : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
     return mk(r0, r1);
   }
+  // The same reduction with the final canonicalisation as selects: the 3-word chain leaves
+  // r < 2^64 with r >= p only if r_hi == 0xffffffff and r_lo != 0, and then r - p = r_lo - 1.
+  __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 c, m, h;\n\t"
+        "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
+        "madc.hi.cc.u32  %1, %4, 0xffffffff, %3;\n\t"
+        "addc.u32        c, 0, 0;\n\t"
+        "sub.cc.u32      %0, %0, %5;\n\t"
+        "subc.cc.u32     %1, %1, 0;\n\t"
+        "subc.u32        c, c, 0;\n\t"
+        "neg.s32         m, c;\n\t"
+        "shr.s32         h, c, 31;\n\t"
+        "add.cc.u32      %0, %0, m;\n\t"
+        "addc.u32        %1, %1, h;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+    const bool big = (r1 == 0xFFFFFFFFu) & (r0 != 0u);
+    return mk(big ? r0 - 1u : r0, big ? 0u : r1);
+  }
   // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
   __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
     // ptxas expands mul.lo.u64 / mul.hi.u64 into IMAD.WIDE.U32 chains with carry predicates
     const uint64_t lo = a * b, hi = __umul64hi(a, b);
     return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  __device__ __forceinline__ static uint64_t mul_m(uint64_t a, uint64_t b) {
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4_m(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
   }
   __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
 
@@ -212,16 +252,16 @@ struct FieldGold {
   }
   // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
   __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
-    const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
-    const uint64_t d = sub_c(u, v);   // canonical
-    u = mul(s, si);
+    const uint64_t s = add_c_m(u, v);   // u + v < 2p: one correction, result weak
+    const uint64_t d = sub_c(u, v);     // canonical
+    u = mul_m(s, si);
     v = d;
   }
   __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
-    const uint64_t s = add_c(u, v);
+    const uint64_t s = add_c_m(u, v);
     const uint64_t d = sub_c(u, v);
-    u = mul(s, si_k);
-    v = mul(d, k);
+    u = mul_m(s, si_k);
+    v = mul_m(d, k);
   }
   __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
   __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {

@@ -418,6 +418,532 @@ struct FieldGoldW2 {  // experiment: W + FMA-pipe borrow corrections + opaque-ze
   }
 };
 
+struct FieldGoldG3 {  // experiment: select-based canonicalisation (ALU-only)
+  using T = uint64_t;
+  using Tw = uint64_t;
+  static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
+  static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
+
+  // All helpers work on 32-bit halves with explicit PTX carry chains.  A wrap-around correction
+  // (+-EPS when a 64-bit add/sub carried/borrowed) is applied arithmetically, never by setp /
+  // selp / predication: after a subtract chain `subc.u32 m, 0, 0` yields m = -borrow (0 or
+  // 0xffffffff = EPS's low word) and the correction is one more subtract chain; after an add
+  // chain `addc.u32 m, 0, 0` yields the carry and `mad.lo.cc m * EPS` adds the correction.  (PTX
+  // carry flags are the hardware carry: after an add, `subc m, 0, 0` gives carry - 1, NOT -carry,
+  // so add and subtract chains are never mixed.)  ptxas maps the materialisations to IMAD.X /
+  // IMAD on the FMA pipe, which offloads the saturated ALU pipe
+  // (profiles/r01c_ncu_full_k_block.txt: the predicated form spent ~11 SEL/ISETP/PLOP3 per modmul).
+  __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+  __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+  // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS;
+  // a + b - 2^64 + EPS <= (2^64-1) + (p-1) - 2^64 + EPS = 2^64 - 2: no second carry.  Weak result.
+  __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
+    uint32_t s0, s1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "add.cc.u32  %0, %2, %4;\n\t"
+        "addc.cc.u32 %1, %3, %5;\n\t"
+        "addc.u32    m, 0, 0;\n\t"                 // m = carry (0/1)
+        "mad.lo.cc.u32 %0, m, 0xffffffff, %0;\n\t" // + EPS * carry
+        "addc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(s0), "=&r"(s1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(s0, s1);
+  }
+  // a - b mod p for a any 64-bit value and b < p: on a borrow subtract EPS; the wrapped value is
+  // a - b + 2^64 >= 2^64 - p + 1 > EPS, so no second borrow.  Canonical if a is canonical.
+  __device__ __forceinline__ static uint64_t sub_c(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"        // m = -borrow
+        "sub.cc.u32  %0, %0, m;\n\t"      // - EPS
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // a - b mod p for any 64-bit a, b: up to two borrow corrections (the second only if
+  // b > a + p - 2^64 + EPS, i.e. both were large); result a - b + {0, p, 2p}, weakly reduced.
+  __device__ __forceinline__ static uint64_t sub_w(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.cc.u32 %1, %1, 0;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
+  //   V = (t1:t0) + t2 EPS - t3 as a 3-word signed value c 2^64 + (r1:r0), c in {-1, 0, 1}
+  //       (V in (-2^32, 2^65 - 2^33]);
+  //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
+  //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
+  //   canonicalise: u = r + EPS carries iff r >= p; then r += EPS * carry (mod 2^64) = r - p.
+  __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 c, m, h;\n\t"
+        "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
+        "madc.hi.cc.u32  %1, %4, 0xffffffff, %3;\n\t"
+        "addc.u32        c, 0, 0;\n\t"
+        "sub.cc.u32      %0, %0, %5;\n\t"
+        "subc.cc.u32     %1, %1, 0;\n\t"
+        "subc.u32        c, c, 0;\n\t"
+        "neg.s32         m, c;\n\t"
+        "shr.s32         h, c, 31;\n\t"
+        "add.cc.u32      %0, %0, m;\n\t"
+        "addc.u32        %1, %1, h;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+    // r >= p  <=>  r_hi == 0xffffffff and r_lo != 0, and then r - p = r_lo - 1
+    const bool big = (r1 == 0xFFFFFFFFu) & (r0 != 0u);
+    return mk(big ? r0 - 1u : r0, big ? 0u : r1);
+  }
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+    // ptxas expands mul.lo.u64 / mul.hi.u64 into IMAD.WIDE.U32 chains with carry predicates
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
+
+  // forward a: inputs weak; t = s y canonical -> single corrections
+  __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(y, s);
+    const uint64_t X = x;
+    x = add_c(X, t);
+    y = sub_c(X, t);
+  }
+  // forward b: t = s x canonical; t + y single correction; t - y with weak y needs two
+  __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(x, s);
+    const uint64_t Y = y;
+    x = add_c(Y, t);
+    y = sub_w(t, Y);
+  }
+  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
+  __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
+    const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
+    const uint64_t d = sub_c(u, v);   // canonical
+    u = mul(s, si);
+    v = d;
+  }
+  __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
+    const uint64_t s = add_c(u, v);
+    const uint64_t d = sub_c(u, v);
+    u = mul(s, si_k);
+    v = mul(d, k);
+  }
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
+    return mul(mul(a, b), k);
+  }
+};
+
+struct FieldGoldG4 {  // experiment: G3 + select-based add correction
+  using T = uint64_t;
+  using Tw = uint64_t;
+  static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
+  static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
+
+  // All helpers work on 32-bit halves with explicit PTX carry chains.  A wrap-around correction
+  // (+-EPS when a 64-bit add/sub carried/borrowed) is applied arithmetically, never by setp /
+  // selp / predication: after a subtract chain `subc.u32 m, 0, 0` yields m = -borrow (0 or
+  // 0xffffffff = EPS's low word) and the correction is one more subtract chain; after an add
+  // chain `addc.u32 m, 0, 0` yields the carry and `mad.lo.cc m * EPS` adds the correction.  (PTX
+  // carry flags are the hardware carry: after an add, `subc m, 0, 0` gives carry - 1, NOT -carry,
+  // so add and subtract chains are never mixed.)  ptxas maps the materialisations to IMAD.X /
+  // IMAD on the FMA pipe, which offloads the saturated ALU pipe
+  // (profiles/r01c_ncu_full_k_block.txt: the predicated form spent ~11 SEL/ISETP/PLOP3 per modmul).
+  __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+  __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+  // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS;
+  // a + b - 2^64 + EPS <= (2^64-1) + (p-1) - 2^64 + EPS = 2^64 - 2: no second carry.  Weak result.
+  __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
+    uint32_t s0, s1, c;
+    asm("add.cc.u32  %0, %3, %5;\n\t"
+        "addc.cc.u32 %1, %4, %6;\n\t"
+        "addc.u32    %2, 0, 0;"
+        : "=r"(s0), "=r"(s1), "=r"(c) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    // + EPS on a carry: lo + 2^32 - 1 = (lo - 1) with a carry into hi unless lo == 0
+    if (c) {
+      const bool z = s0 == 0u;
+      s1 = z ? s1 : s1 + 1u;
+      s0 = s0 - 1u;
+    }
+    return mk(s0, s1);
+  }
+  // a - b mod p for a any 64-bit value and b < p: on a borrow subtract EPS; the wrapped value is
+  // a - b + 2^64 >= 2^64 - p + 1 > EPS, so no second borrow.  Canonical if a is canonical.
+  __device__ __forceinline__ static uint64_t sub_c(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"        // m = -borrow
+        "sub.cc.u32  %0, %0, m;\n\t"      // - EPS
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // a - b mod p for any 64-bit a, b: up to two borrow corrections (the second only if
+  // b > a + p - 2^64 + EPS, i.e. both were large); result a - b + {0, p, 2p}, weakly reduced.
+  __device__ __forceinline__ static uint64_t sub_w(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.cc.u32 %1, %1, 0;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
+  //   V = (t1:t0) + t2 EPS - t3 as a 3-word signed value c 2^64 + (r1:r0), c in {-1, 0, 1}
+  //       (V in (-2^32, 2^65 - 2^33]);
+  //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
+  //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
+  //   canonicalise: u = r + EPS carries iff r >= p; then r += EPS * carry (mod 2^64) = r - p.
+  __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 c, m, h;\n\t"
+        "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
+        "madc.hi.cc.u32  %1, %4, 0xffffffff, %3;\n\t"
+        "addc.u32        c, 0, 0;\n\t"
+        "sub.cc.u32      %0, %0, %5;\n\t"
+        "subc.cc.u32     %1, %1, 0;\n\t"
+        "subc.u32        c, c, 0;\n\t"
+        "neg.s32         m, c;\n\t"
+        "shr.s32         h, c, 31;\n\t"
+        "add.cc.u32      %0, %0, m;\n\t"
+        "addc.u32        %1, %1, h;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+    // r >= p  <=>  r_hi == 0xffffffff and r_lo != 0, and then r - p = r_lo - 1
+    const bool big = (r1 == 0xFFFFFFFFu) & (r0 != 0u);
+    return mk(big ? r0 - 1u : r0, big ? 0u : r1);
+  }
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+    // ptxas expands mul.lo.u64 / mul.hi.u64 into IMAD.WIDE.U32 chains with carry predicates
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
+
+  // forward a: inputs weak; t = s y canonical -> single corrections
+  __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(y, s);
+    const uint64_t X = x;
+    x = add_c(X, t);
+    y = sub_c(X, t);
+  }
+  // forward b: t = s x canonical; t + y single correction; t - y with weak y needs two
+  __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(x, s);
+    const uint64_t Y = y;
+    x = add_c(Y, t);
+    y = sub_w(t, Y);
+  }
+  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
+  __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
+    const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
+    const uint64_t d = sub_c(u, v);   // canonical
+    u = mul(s, si);
+    v = d;
+  }
+  __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
+    const uint64_t s = add_c(u, v);
+    const uint64_t d = sub_c(u, v);
+    u = mul(s, si_k);
+    v = mul(d, k);
+  }
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
+    return mul(mul(a, b), k);
+  }
+};
+
+struct FieldGoldG5 {  // experiment: forward = G4, inverse = current mask arithmetic
+  using T = uint64_t;
+  using Tw = uint64_t;
+  static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
+  static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
+
+  // All helpers work on 32-bit halves with explicit PTX carry chains.  A wrap-around correction
+  // (+-EPS when a 64-bit add/sub carried/borrowed) is applied arithmetically, never by setp /
+  // selp / predication: after a subtract chain `subc.u32 m, 0, 0` yields m = -borrow (0 or
+  // 0xffffffff = EPS's low word) and the correction is one more subtract chain; after an add
+  // chain `addc.u32 m, 0, 0` yields the carry and `mad.lo.cc m * EPS` adds the correction.  (PTX
+  // carry flags are the hardware carry: after an add, `subc m, 0, 0` gives carry - 1, NOT -carry,
+  // so add and subtract chains are never mixed.)  ptxas maps the materialisations to IMAD.X /
+  // IMAD on the FMA pipe, which offloads the saturated ALU pipe
+  // (profiles/r01c_ncu_full_k_block.txt: the predicated form spent ~11 SEL/ISETP/PLOP3 per modmul).
+  __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+  __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+  // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS;
+  // a + b - 2^64 + EPS <= (2^64-1) + (p-1) - 2^64 + EPS = 2^64 - 2: no second carry.  Weak result.
+  __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
+    uint32_t s0, s1, c;
+    asm("add.cc.u32  %0, %3, %5;\n\t"
+        "addc.cc.u32 %1, %4, %6;\n\t"
+        "addc.u32    %2, 0, 0;"
+        : "=r"(s0), "=r"(s1), "=r"(c) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    // + EPS on a carry: lo + 2^32 - 1 = (lo - 1) with a carry into hi unless lo == 0
+    if (c) {
+      const bool z = s0 == 0u;
+      s1 = z ? s1 : s1 + 1u;
+      s0 = s0 - 1u;
+    }
+    return mk(s0, s1);
+  }
+  // a - b mod p for a any 64-bit value and b < p: on a borrow subtract EPS; the wrapped value is
+  // a - b + 2^64 >= 2^64 - p + 1 > EPS, so no second borrow.  Canonical if a is canonical.
+  __device__ __forceinline__ static uint64_t sub_c(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"        // m = -borrow
+        "sub.cc.u32  %0, %0, m;\n\t"      // - EPS
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // a - b mod p for any 64-bit a, b: up to two borrow corrections (the second only if
+  // b > a + p - 2^64 + EPS, i.e. both were large); result a - b + {0, p, 2p}, weakly reduced.
+  __device__ __forceinline__ static uint64_t sub_w(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.cc.u32 %1, %1, 0;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
+  //   V = (t1:t0) + t2 EPS - t3 as a 3-word signed value c 2^64 + (r1:r0), c in {-1, 0, 1}
+  //       (V in (-2^32, 2^65 - 2^33]);
+  //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
+  //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
+  //   canonicalise: u = r + EPS carries iff r >= p; then r += EPS * carry (mod 2^64) = r - p.
+  __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 c, m, h;\n\t"
+        "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
+        "madc.hi.cc.u32  %1, %4, 0xffffffff, %3;\n\t"
+        "addc.u32        c, 0, 0;\n\t"
+        "sub.cc.u32      %0, %0, %5;\n\t"
+        "subc.cc.u32     %1, %1, 0;\n\t"
+        "subc.u32        c, c, 0;\n\t"
+        "neg.s32         m, c;\n\t"
+        "shr.s32         h, c, 31;\n\t"
+        "add.cc.u32      %0, %0, m;\n\t"
+        "addc.u32        %1, %1, h;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+    // r >= p  <=>  r_hi == 0xffffffff and r_lo != 0, and then r - p = r_lo - 1
+    const bool big = (r1 == 0xFFFFFFFFu) & (r0 != 0u);
+    return mk(big ? r0 - 1u : r0, big ? 0u : r1);
+  }
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+    // ptxas expands mul.lo.u64 / mul.hi.u64 into IMAD.WIDE.U32 chains with carry predicates
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
+
+  // forward a: inputs weak; t = s y canonical -> single corrections
+  __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(y, s);
+    const uint64_t X = x;
+    x = add_c(X, t);
+    y = sub_c(X, t);
+  }
+  // forward b: t = s x canonical; t + y single correction; t - y with weak y needs two
+  __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(x, s);
+    const uint64_t Y = y;
+    x = add_c(Y, t);
+    y = sub_w(t, Y);
+  }
+  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
+  __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
+    const uint64_t s = FieldGold::add_c(u, v);
+    const uint64_t d = FieldGold::sub_c(u, v);
+    u = FieldGold::mul(s, si);
+    v = d;
+  }
+  __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
+    const uint64_t s = add_c(u, v);
+    const uint64_t d = sub_c(u, v);
+    u = mul(s, si_k);
+    v = mul(d, k);
+  }
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
+    return mul(mul(a, b), k);
+  }
+};
+
+struct FieldGoldG6 {  // experiment: forward = G4, inverse = mask add + select canonicalisation
+  using T = uint64_t;
+  using Tw = uint64_t;
+  static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
+  static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
+
+  // All helpers work on 32-bit halves with explicit PTX carry chains.  A wrap-around correction
+  // (+-EPS when a 64-bit add/sub carried/borrowed) is applied arithmetically, never by setp /
+  // selp / predication: after a subtract chain `subc.u32 m, 0, 0` yields m = -borrow (0 or
+  // 0xffffffff = EPS's low word) and the correction is one more subtract chain; after an add
+  // chain `addc.u32 m, 0, 0` yields the carry and `mad.lo.cc m * EPS` adds the correction.  (PTX
+  // carry flags are the hardware carry: after an add, `subc m, 0, 0` gives carry - 1, NOT -carry,
+  // so add and subtract chains are never mixed.)  ptxas maps the materialisations to IMAD.X /
+  // IMAD on the FMA pipe, which offloads the saturated ALU pipe
+  // (profiles/r01c_ncu_full_k_block.txt: the predicated form spent ~11 SEL/ISETP/PLOP3 per modmul).
+  __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+  __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+
+  // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS;
+  // a + b - 2^64 + EPS <= (2^64-1) + (p-1) - 2^64 + EPS = 2^64 - 2: no second carry.  Weak result.
+  __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
+    uint32_t s0, s1, c;
+    asm("add.cc.u32  %0, %3, %5;\n\t"
+        "addc.cc.u32 %1, %4, %6;\n\t"
+        "addc.u32    %2, 0, 0;"
+        : "=r"(s0), "=r"(s1), "=r"(c) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    // + EPS on a carry: lo + 2^32 - 1 = (lo - 1) with a carry into hi unless lo == 0
+    if (c) {
+      const bool z = s0 == 0u;
+      s1 = z ? s1 : s1 + 1u;
+      s0 = s0 - 1u;
+    }
+    return mk(s0, s1);
+  }
+  // a - b mod p for a any 64-bit value and b < p: on a borrow subtract EPS; the wrapped value is
+  // a - b + 2^64 >= 2^64 - p + 1 > EPS, so no second borrow.  Canonical if a is canonical.
+  __device__ __forceinline__ static uint64_t sub_c(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"        // m = -borrow
+        "sub.cc.u32  %0, %0, m;\n\t"      // - EPS
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // a - b mod p for any 64-bit a, b: up to two borrow corrections (the second only if
+  // b > a + p - 2^64 + EPS, i.e. both were large); result a - b + {0, p, 2p}, weakly reduced.
+  __device__ __forceinline__ static uint64_t sub_w(uint64_t a, uint64_t b) {
+    uint32_t d0, d1;
+    asm("{\n\t.reg .u32 m;\n\t"
+        "sub.cc.u32  %0, %2, %4;\n\t"
+        "subc.cc.u32 %1, %3, %5;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.cc.u32 %1, %1, 0;\n\t"
+        "subc.u32    m, 0, 0;\n\t"
+        "sub.cc.u32  %0, %0, m;\n\t"
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(d0), "=&r"(d1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(d0, d1);
+  }
+  // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
+  //   V = (t1:t0) + t2 EPS - t3 as a 3-word signed value c 2^64 + (r1:r0), c in {-1, 0, 1}
+  //       (V in (-2^32, 2^65 - 2^33]);
+  //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
+  //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
+  //   canonicalise: u = r + EPS carries iff r >= p; then r += EPS * carry (mod 2^64) = r - p.
+  __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 c, m, h;\n\t"
+        "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
+        "madc.hi.cc.u32  %1, %4, 0xffffffff, %3;\n\t"
+        "addc.u32        c, 0, 0;\n\t"
+        "sub.cc.u32      %0, %0, %5;\n\t"
+        "subc.cc.u32     %1, %1, 0;\n\t"
+        "subc.u32        c, c, 0;\n\t"
+        "neg.s32         m, c;\n\t"
+        "shr.s32         h, c, 31;\n\t"
+        "add.cc.u32      %0, %0, m;\n\t"
+        "addc.u32        %1, %1, h;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+    // r >= p  <=>  r_hi == 0xffffffff and r_lo != 0, and then r - p = r_lo - 1
+    const bool big = (r1 == 0xFFFFFFFFu) & (r0 != 0u);
+    return mk(big ? r0 - 1u : r0, big ? 0u : r1);
+  }
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+    // ptxas expands mul.lo.u64 / mul.hi.u64 into IMAD.WIDE.U32 chains with carry predicates
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
+
+  // forward a: inputs weak; t = s y canonical -> single corrections
+  __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(y, s);
+    const uint64_t X = x;
+    x = add_c(X, t);
+    y = sub_c(X, t);
+  }
+  // forward b: t = s x canonical; t + y single correction; t - y with weak y needs two
+  __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(x, s);
+    const uint64_t Y = y;
+    x = add_c(Y, t);
+    y = sub_w(t, Y);
+  }
+  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
+  __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
+    const uint64_t s = FieldGold::add_c(u, v);
+    const uint64_t d = FieldGold::sub_c(u, v);
+    u = mul(s, si);
+    v = d;
+  }
+  __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
+    const uint64_t s = add_c(u, v);
+    const uint64_t d = sub_c(u, v);
+    u = mul(s, si_k);
+    v = mul(d, k);
+  }
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
+    return mul(mul(a, b), k);
+  }
+};
+
 }  // namespace fcirc
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { fprintf(stderr, "CUDA %s line %d\n", cudaGetErrorString(e_), __LINE__); return 1; } } while (0)
@@ -542,5 +1068,9 @@ int main() {
   rc |= run<FieldGold>("mask corrections (FieldGold, current)", nsm);
   rc |= run<FieldGoldW>("mad.wide corrections (FieldGoldW)", nsm);
   rc |= run<FieldGoldW2>("W + FMA borrow corrections + opaque zero (FieldGoldW2)", nsm);
+  rc |= run<FieldGoldG3>("select-based canonicalisation (FieldGoldG3)", nsm);
+  rc |= run<FieldGoldG4>("G3 + select-based add correction (FieldGoldG4)", nsm);
+  rc |= run<FieldGoldG5>("forward G4, inverse current (FieldGoldG5)", nsm);
+  rc |= run<FieldGoldG6>("forward G4, inverse mask add + select canon (FieldGoldG6)", nsm);
   return rc;
 }

@@ -95,7 +95,7 @@ def run(text: str, nout: int, inputs):
 def helper(src: str, fn: str):
     """Python callable on 64-bit values for FieldGold.<fn> (add_c, sub_c, sub_w) or reduce4."""
     text, nout, nin = extract(src, fn)
-    if fn == "reduce4":
+    if fn.startswith("reduce4"):
         def f(t0, t1, t2, t3):
             r0, r1 = run(text, nout, [t0, t1, t2, t3])
             return r0 | (r1 << 32)
