@@ -13,7 +13,9 @@
  *        18446744069414584321 = 2^64 - 2^32 + 1  "Goldilocks"  (uint64_t)
  *    The element type of a, b, c follows p: uint32_t for the three 32-bit primes, uint64_t for
  *    Goldilocks.  Inputs must be canonical residues in [0, p) (precondition, not checked on the
- *    device); outputs are canonical.
+ *    device unless the environment sets FCIRC_CHECK_INPUTS=1: then fcirc_matvec / fcirc_polymul
+ *    first count non-canonical inputs, synchronise the stream and return FCIRC_EINVAL if there
+ *    are any); outputs are canonical.
  *  - Layout: row-major [batch][len], contiguous; instance k starts at element k*len.
  *  - Data pointers are DEVICE pointers owned by the caller, except the *_host entry points,
  *    whose data pointers are HOST pointers (pinned memory gives full PCIe bandwidth).

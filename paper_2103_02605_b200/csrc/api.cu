@@ -69,7 +69,29 @@ DevPlan::~DevPlan() {
 
 static std::mutex g_mu;
 static std::mutex g_host_mu;
-static std::map<std::tuple<int, uint64_t, uint64_t, int>, std::shared_ptr<DevPlan>> g_plans;
+// plan cache keyed by (device, p, f, log2 n), least-recently-used eviction beyond kMaxPlans entries or
+// kMaxPlanBytes of device tables (callers with a new f per call would otherwise grow it without
+// bound); evicted tables are freed by the last shared_ptr owner (cudaFree synchronises the device).
+struct PlanEntry {
+  std::shared_ptr<DevPlan> plan;
+  uint64_t last_use = 0;
+  size_t bytes = 0;
+};
+static std::map<std::tuple<int, uint64_t, uint64_t, int>, PlanEntry> g_plans;
+static uint64_t g_plan_tick = 0;
+static size_t g_plan_bytes = 0;
+static constexpr size_t kMaxPlans = 64;
+static constexpr size_t kMaxPlanBytes = (size_t)2 << 30;
+
+static void evict_plans_locked() {
+  while (g_plans.size() > kMaxPlans || (g_plan_bytes > kMaxPlanBytes && g_plans.size() > 1)) {
+    auto victim = g_plans.begin();
+    for (auto it = g_plans.begin(); it != g_plans.end(); ++it)
+      if (it->second.last_use < victim->second.last_use) victim = it;
+    g_plan_bytes -= victim->second.bytes;
+    g_plans.erase(victim);
+  }
+}
 
 static TwU32 shoup_pair(uint64_t w, uint64_t p) {
   TwU32 t;
@@ -83,16 +105,22 @@ static int get_plan(int dev, uint64_t p, uint64_t f, int L, std::shared_ptr<DevP
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_plans.find(key);
-    if (it != g_plans.end()) { *out = it->second; return FCIRC_OK; }
+    if (it != g_plans.end()) {
+      it->second.last_use = ++g_plan_tick;
+      *out = it->second.plan;
+      return FCIRC_OK;
+    }
   }
   auto dp = std::make_shared<DevPlan>();
   int st = build_host_plan(p, f, L, &dp->hp);
   if (st != FCIRC_OK) return st;
   const PrimeInfo* pi = prime_info(p);
   const size_t n = dp->hp.s.size();
+  size_t bytes = 0;
   if (!pi->wide) {
     std::vector<TwU32> hf(n), hi(n);
     for (size_t i = 0; i < n; ++i) { hf[i] = shoup_pair(dp->hp.s[i], p); hi[i] = shoup_pair(dp->hp.sinv[i], p); }
+    bytes = 2 * n * sizeof(TwU32);
     if (cudaMalloc(&dp->twf, n * sizeof(TwU32)) != cudaSuccess) return FCIRC_ENOMEM;
     if (cudaMalloc(&dp->twi, n * sizeof(TwU32)) != cudaSuccess) return FCIRC_ENOMEM;
     if (cudaMemcpy(dp->twf, hf.data(), n * sizeof(TwU32), cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
@@ -100,6 +128,7 @@ static int get_plan(int dev, uint64_t p, uint64_t f, int L, std::shared_ptr<DevP
     dp->last_si32 = shoup_pair(dp->hp.last_si, p);
     dp->last_k32 = shoup_pair(dp->hp.K, p);
   } else {
+    bytes = 2 * n * 8;
     if (cudaMalloc(&dp->twf, n * 8) != cudaSuccess) return FCIRC_ENOMEM;
     if (cudaMalloc(&dp->twi, n * 8) != cudaSuccess) return FCIRC_ENOMEM;
     if (cudaMemcpy(dp->twf, dp->hp.s.data(), n * 8, cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
@@ -109,8 +138,14 @@ static int get_plan(int dev, uint64_t p, uint64_t f, int L, std::shared_ptr<DevP
   }
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_plans.find(key);
-  if (it != g_plans.end()) { *out = it->second; return FCIRC_OK; }  // another thread won
-  g_plans[key] = dp;
+  if (it != g_plans.end()) {  // another thread won
+    it->second.last_use = ++g_plan_tick;
+    *out = it->second.plan;
+    return FCIRC_OK;
+  }
+  g_plans[key] = PlanEntry{dp, ++g_plan_tick, bytes};
+  g_plan_bytes += bytes;
+  evict_plans_locked();
   *out = dp;
   return FCIRC_OK;
 }
@@ -179,6 +214,36 @@ static int ilog2_exact(int64_t n) {
   return L;
 }
 
+// ------------------------------------------------------------------------------------------
+// optional input validation (FCIRC_CHECK_INPUTS=1): inputs must be canonical residues (< p); the
+// product path does not check this on the device.  In checking mode a counting kernel runs first
+// and the call synchronises the stream and returns FCIRC_EINVAL if any element is >= p.
+// ------------------------------------------------------------------------------------------
+template <class E>
+__global__ void k_count_noncanonical(const E* __restrict__ x, int64_t count, uint64_t p,
+                                     unsigned long long* __restrict__ bad) {
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    local += (uint64_t)x[i] >= p;
+  if (local) atomicAdd(bad, local);
+}
+
+static int check_canonical(uint64_t p, bool wide, const void* x, int64_t count, cudaStream_t st) {
+  static const bool on = knob("CHECK_INPUTS", 0) != 0;
+  if (!on || count <= 0) return FCIRC_OK;
+  unsigned long long* d = nullptr;
+  unsigned long long h = 0;
+  if (cudaMallocAsync((void**)&d, sizeof h, st) != cudaSuccess) return FCIRC_ENOMEM;
+  cudaMemsetAsync(d, 0, sizeof h, st);
+  const unsigned blocks = (unsigned)std::min<int64_t>((count + 255) / 256, 148 * 8);
+  if (wide) k_count_noncanonical<uint64_t><<<blocks, 256, 0, st>>>((const uint64_t*)x, count, p, d);
+  else k_count_noncanonical<uint32_t><<<blocks, 256, 0, st>>>((const uint32_t*)x, count, p, d);
+  cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return FCIRC_ECUDA;
+  return h ? FCIRC_EINVAL : FCIRC_OK;
+}
+
 // plan lookup + dispatch of one batched product (no argument validation; callers validate)
 static int matvec_core(uint64_t p, uint64_t f, const void* a, const void* b, void* c, int L, int64_t batch,
                        cudaStream_t st, const EmbedIO& io) {
@@ -211,6 +276,9 @@ static int matvec_impl(uint64_t p, uint64_t f, const void* a, const void* b, voi
   if (L > pi->two_adicity || L > max_log_n(pi->wide)) return FCIRC_ESIZE;
   const size_t bytes = (size_t)n * (size_t)batch * es;
   if (overlaps(c, bytes, a, bytes) || overlaps(c, bytes, b, bytes)) return FCIRC_EINVAL;
+  int rc = check_canonical(p, pi->wide, a, n * batch, st);
+  if (rc == FCIRC_OK) rc = check_canonical(p, pi->wide, b, n * batch, st);
+  if (rc) return rc;
   return matvec_core(p, f, a, b, c, L, batch, st, EmbedIO{});
 }
 
@@ -398,6 +466,9 @@ int fcirc_polymul(uint64_t p, const void* a, int64_t na, const void* b, int64_t 
     return FCIRC_EINVAL;
   const int64_t L = next_pow2(nc);
   if (ilog2_exact(L) > pi->two_adicity || ilog2_exact(L) > max_log_n(pi->wide)) return FCIRC_ESIZE;
+  int rc = check_canonical(p, pi->wide, a, na * batch, (cudaStream_t)stream);
+  if (rc == FCIRC_OK) rc = check_canonical(p, pi->wide, b, nb * batch, (cudaStream_t)stream);
+  if (rc) return rc;
   return polymul_impl(p, a, na, b, nb, c, batch, (cudaStream_t)stream);
 }
 
@@ -477,6 +548,7 @@ int fcirc_release_cache(void) {
   cudaDeviceSynchronize();
   std::lock_guard<std::mutex> lk(g_mu);
   g_plans.clear();
+  g_plan_bytes = 0;
   for (auto& kv : g_ws)
     if (kv.second.ptr) cudaFree(kv.second.ptr);
   g_ws.clear();

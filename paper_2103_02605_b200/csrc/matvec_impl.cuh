@@ -59,14 +59,11 @@ static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t s
   // (cap 128: without a floor ptxas spends ~190 registers and halves the resident warps)
   constexpr int MINB = (T * IPC < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / (T * IPC) : 1;
   auto kern = k_block<F, M, R, IPC, MINB, EMB, TWS>;
-  if (smem > 48 * 1024) {
-    static bool once = false;  // attribute set per kernel instantiation
-    if (!once) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return FCIRC_ECUDA;
-      once = true;
-    }
-  }
+  // opt-in shared memory, once per instantiation (thread-safe static initialisation)
+  static const bool attr_ok =
+      smem <= 48 * 1024 ||
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+  if (!attr_ok) return FCIRC_ECUDA;
   const int64_t batch = args.units >> args.k;
   const int64_t grid = ((batch + IPC - 1) / IPC) << args.k;
   prof_begin(args.k == 0 ? 0 : 1, st);
@@ -92,14 +89,10 @@ static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStr
   const size_t smem = (size_t)(1 << K) * W * sizeof(E);
   constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
   auto kern = k_cols<F, K, R, W, INV, MINB, EMB>;
-  if (smem > 48 * 1024) {
-    static bool once = false;
-    if (!once) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return FCIRC_ECUDA;
-      once = true;
-    }
-  }
+  static const bool attr_ok =
+      smem <= 48 * 1024 ||
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+  if (!attr_ok) return FCIRC_ECUDA;
   args.colblocks = args.m / W;
   args.units = instances * args.colblocks;
   dim3 grid((unsigned)args.units, INV ? 1 : 2);
@@ -147,16 +140,16 @@ static int launch_cols_tma(const F& fld, ColArgs<F> args, int64_t instances, cud
   const size_t smem = (size_t)3 * (1 << K) * W * sizeof(E) + 16 + 128;
   constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
   auto kern = k_cols_tma<F, K, R, W, INV, MINB>;
-  static int occ = -1;   // resident CTAs per SM (per instantiation)
-  if (occ < 0) {
+  // resident CTAs per SM, once per instantiation (thread-safe static initialisation; 0 = error)
+  static const int occ = [&] {
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return FCIRC_ECUDA;
+      return 0;
     int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem) != cudaSuccess || o < 1)
-      return FCIRC_ECUDA;
-    occ = o;
-  }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem) != cudaSuccess) return 0;
+    return o;
+  }();
+  if (occ < 1) return FCIRC_ECUDA;
   args.colblocks = args.m / W;
   args.units = instances * args.colblocks;
   CUtensorMap m0, m1;

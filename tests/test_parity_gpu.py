@@ -9,6 +9,8 @@ Coverage rules:
   * polymul: sampled coefficients + Schwartz-Zippel; bigint: the full product vs Python ints and
     the oracle's Karatsuba.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -294,3 +296,71 @@ def test_config_C5_bigint():
         assert _to_int(z[k]) == _to_int(inp["x"][k]) * _to_int(inp["y"][k]), k
     # and against the oracle's independent Karatsuba, word for word
     assert np.array_equal(z[0], oracle.bigint_mul(inp["x"][0], inp["y"][0]))
+
+
+# ---------------------------------------------------------------------------------- runtime
+
+def test_plan_cache_eviction_many_f():
+    """More distinct (p, f, n) plans than the cache keeps (64): evicted plans are rebuilt and every
+    result stays exact (no stale or freed twist table is used)."""
+    rng = np.random.default_rng(123)
+    for i in range(80):
+        p = P998 if i % 2 else GOLDILOCKS
+        inp = synth.matvec_inputs(p, 1 << 9, 2, seed=int(rng.integers(1 << 30)))
+        c = run_matvec(inp)
+        if i % 10 == 0 or i > 70:
+            check_full(inp, c)
+
+
+def test_concurrent_host_threads_and_streams():
+    """Two host threads, each on its own stream, issue products concurrently (plan cache and
+    workspace pool are shared and mutex-guarded)."""
+    import threading
+    results, errors = {}, []
+
+    def work(tid):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for j in range(6):
+                    p = GOLDILOCKS if (tid + j) % 2 else P998
+                    inp = synth.matvec_inputs(p, 1 << (14 + j % 3), 2, seed=1000 * tid + j)
+                    a, b = _dev(inp["a"]), _dev(inp["b"])
+                    c = fc.matvec(a, b, inp["f"], p, stream=s)
+                    s.synchronize()
+                    results[(tid, j)] = (inp, _host(c))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    ts = [threading.Thread(target=work, args=(t,)) for t in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for (tid, j), (inp, c) in results.items():
+        check_sampled(inp, c, [0, 1], count=256, thetas=1)
+
+
+def test_check_inputs_mode_rejects_noncanonical():
+    """FCIRC_CHECK_INPUTS=1 (debug mode): an input >= p is reported as FCIRC_EINVAL instead of
+    producing a silently wrong product.  Runs in a subprocess (the knob is read once)."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, paper_2103_02605_b200 as fc, synth
+inp = synth.matvec_inputs(synth.P998, 1 << 12, 2, seed=5)
+a = torch.from_numpy(inp["a"]).cuda(); b = torch.from_numpy(inp["b"]).cuda()
+fc.matvec(a, b, inp["f"], synth.P998)                       # canonical: accepted
+bad = inp["a"].copy(); bad[1, 77] = synth.P998              # == p: not canonical
+a = torch.from_numpy(bad).cuda()
+try:
+    fc.matvec(a, b, inp["f"], synth.P998)
+    print("accepted")
+except fc.FcircError as e:
+    print("rejected", e.code)
+'''
+    env = dict(os.environ, FCIRC_CHECK_INPUTS="1")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert "rejected -1" in out.stdout, out.stdout + out.stderr
