@@ -394,6 +394,21 @@ def run_fcirc(args):
         wl.step()
     torch.cuda.synchronize()
 
+    # ---- CUDA graph of one step (launch-bound configurations: the step is shorter than the host
+    # time to issue it, so the timed region replays a captured graph instead of calling the API)
+    use_graph = args.graph == "on" or (args.graph == "auto" and (wl.elems < (1 << 20) or wl.kind == "bigint"))
+    graph = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                wl.step()
+        stream.wait_stream(cap)
+        graph.replay()
+        torch.cuda.synchronize()
+
     # ---- timed region (device time, CUDA events on the launching stream)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
@@ -401,14 +416,23 @@ def run_fcirc(args):
         dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(torch.cuda.current_device())
-    fc.profile_enable(True)
+    fc.profile_enable(not use_graph)
     with sampler:
         ev0.record(stream)
         for _ in range(args.steps):
-            launches += wl.step()
+            if use_graph:
+                graph.replay()
+            else:
+                launches += wl.step()
         ev1.record(stream)
         torch.cuda.synchronize()
     fc.profile_enable(False)
+    if use_graph:   # per-kernel event timing from an un-captured pass of the same steps
+        fc.profile_enable(True)
+        for _ in range(args.steps):
+            launches += wl.step()
+        torch.cuda.synchronize()
+        fc.profile_enable(False)
     prof = fc.profile_read()
     if world > 1:
         dist.barrier()
@@ -479,6 +503,7 @@ def run_fcirc(args):
             "vs_baseline": None, "dtype": width, "data": "synthetic (seeded uniform residues, SURVEY §8(d))",
             "config": wl.config_block(args), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": sampler.summary(), "plan_build_ms": plan_ms,
+            "timing": "CUDA graph replay of the step" if use_graph else "API call per step",
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -497,6 +522,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="replay a CUDA graph of one step in the timed region "
+                         "(auto: launch-bound steps -- fewer than 2^20 elements, or the 14-launch bigint)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

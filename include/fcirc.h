@@ -24,8 +24,11 @@
  *    plan construction and launch errors only; device faults surface at the caller's next
  *    synchronisation.  The first call for a new (device, p, f, n) builds a twist-table plan on
  *    the host and uploads it (synchronous w.r.t. the host, cached afterwards).
- *  - Thread safety: calls may be made concurrently from several host threads; the plan cache
- *    and workspace pool are mutex-guarded.  Concurrent calls on different streams are safe.
+ *  - Thread safety: calls may be made concurrently from several host threads; the plan cache is
+ *    mutex-guarded (LRU, at most 64 plans / 2 GiB of tables).  Scratch memory is allocated
+ *    stream-ordered from the device's default memory pool (cudaMallocAsync / cudaFreeAsync on
+ *    `stream`), so concurrent calls on different streams never share it and a call can be
+ *    captured into a CUDA graph once its plan exists (first call for (p, f, n) outside capture).
  *  - Nothing here ever falls back to a CPU implementation.
  */
 #ifndef FCIRC_H
@@ -152,7 +155,7 @@ int fcirc_plan_table(uint64_t p, uint64_t f, int64_t n, uint64_t* s, uint64_t* s
 int fcirc_profile_enable(int on);
 int fcirc_profile_read(int64_t* counts, double* ms, int nkinds);
 
-/* release all cached plans and workspaces of the current device (for tests / teardown) */
+/* release all cached plans and trim the current device's default memory pool (tests / teardown) */
 int fcirc_release_cache(void);
 
 #ifdef __cplusplus

@@ -151,30 +151,32 @@ static int get_plan(int dev, uint64_t p, uint64_t f, int L, std::shared_ptr<DevP
 }
 
 // ------------------------------------------------------------------------------------------
-// workspace: one grow-only device buffer per (device, stream)
+// workspace: stream-ordered allocations from the device's default memory pool (cudaMallocAsync /
+// cudaFreeAsync on the call's stream).  The pool keeps freed blocks (release threshold raised to
+// the maximum), so after the first call this costs no cudaMalloc; calls on different streams never
+// share scratch; and the allocations are capturable, so a whole product can be recorded in a CUDA
+// graph (bench.py --graph).
 // ------------------------------------------------------------------------------------------
-struct Workspace {
-  void* ptr = nullptr;
-  size_t bytes = 0;
-};
-static std::map<std::tuple<int, void*, int>, Workspace> g_ws;
-
-// tag separates independent buffers of one call (0: matvec b', 1..: application scratch)
-int get_workspace(int dev, void* stream, size_t bytes, void** out, int tag) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  Workspace& w = g_ws[std::make_tuple(dev, stream, tag)];
-  if (w.bytes < bytes) {
-    if (w.ptr) {
-      cudaStreamSynchronize((cudaStream_t)stream);  // previous users on this stream are done
-      cudaFree(w.ptr);
-      w.ptr = nullptr;
-      w.bytes = 0;
+int ws_alloc(int dev, cudaStream_t st, size_t bytes, void** out) {
+  static std::mutex mu;
+  static std::map<int, bool> configured;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!configured[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      configured[dev] = true;
     }
-    if (cudaMalloc(&w.ptr, bytes) != cudaSuccess) return FCIRC_ENOMEM;
-    w.bytes = bytes;
   }
-  *out = w.ptr;
+  if (cudaMallocAsync(out, bytes, st) != cudaSuccess) return FCIRC_ENOMEM;
   return FCIRC_OK;
+}
+
+void ws_free(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
 }
 
 size_t chunk_bytes() {
@@ -364,8 +366,9 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   const size_t need = (size_t)(3 * batch * L) * 4 + (size_t)(2 * batch * ncoef) * 8 + (size_t)(batch * nd) * 4 +
                       (size_t)(batch * nseg) * 4;
   void* ws;
-  int rc = get_workspace(dev, (void*)st, need, &ws, 2);
+  int rc = ws_alloc(dev, st, need, &ws);
   if (rc) return rc;
+  struct Free { void* p; cudaStream_t s; ~Free() { ws_free(p, s); } } free_ws{ws, st};
   uint32_t* r1 = (uint32_t*)ws;
   uint32_t* r2 = r1 + batch * L;
   uint32_t* r3 = r2 + batch * L;
@@ -549,9 +552,10 @@ int fcirc_release_cache(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   g_plans.clear();
   g_plan_bytes = 0;
-  for (auto& kv : g_ws)
-    if (kv.second.ptr) cudaFree(kv.second.ptr);
-  g_ws.clear();
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+    cudaMemPoolTrimTo(pool, 0);
   return FCIRC_OK;
 }
 

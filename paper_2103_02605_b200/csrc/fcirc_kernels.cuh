@@ -448,6 +448,183 @@ k_cols(F fld, ColArgs<F> args) {
 
 
 // ------------------------------------------------------------------------------------------
+// k_cols_fwd2: the forward column pass for a AND b in the same thread (like k_block): each twiddle
+// load serves both splits and every level has twice the independent butterflies per thread, which
+// the Goldilocks column pass needs to hide its carry-chain latency (profiles/r01e: k_cols<fwd>
+// stalled on "wait" at 2.3 per issue vs 1.2 in k_block).
+// ------------------------------------------------------------------------------------------
+template <class F, int K, int R, int W, int MINB = 1, bool EMB = false>
+__global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
+k_cols_fwd2(F fld, ColArgs<F> args) {
+  using T = typename F::T;
+  using Tw = typename F::Tw;
+  using PH = Phases<K, R>;
+  constexpr int NPH = PH::NPH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sma = reinterpret_cast<T*>(smem_raw);
+  T* smb = sma + (1 << K) * W;
+
+  const int c = threadIdx.x % W;
+  const int t = threadIdx.x / W;
+  const int64_t unit = blockIdx.x;
+  const int64_t inst = unit / args.colblocks;
+  const int64_t cb = unit - inst * args.colblocks;
+  const int64_t col = cb * W + c;
+  const int64_t base = inst * args.n + col;
+  const int64_t m = args.m;
+  auto sidx = [&](int row) { return (row ^ ((row >> PH::r) & 7)) * W + c; };
+
+  T xa[R], xb[R];
+  {
+    const int rb = PH::ins_t(0, t);
+    if (!EMB) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int64_t ad = base + (int64_t)(rb + PH::cslot(0, s)) * m;
+        xa[s] = args.src0[ad];
+        xb[s] = args.src1[ad];
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int64_t pos = col + (int64_t)(rb + PH::cslot(0, s)) * m;
+        xa[s] = io_load(args.src0, inst, pos, args.n, false, args.io);
+        xb[s] = io_load(args.src1, inst, pos, args.n, true, args.io);
+      }
+    }
+  }
+#pragma unroll
+  for (int ph = 0; ph < NPH; ++ph) {
+    if (ph > 0) {
+      const int wb = PH::ins_t(ph - 1, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int ad = sidx(wb + PH::cslot(ph - 1, s));
+        sma[ad] = xa[s];
+        smb[ad] = xb[s];
+      }
+      __syncthreads();
+      const int rb = PH::ins_t(ph, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int ad = sidx(rb + PH::cslot(ph, s));
+        xa[s] = sma[ad];
+        xb[s] = smb[ad];
+      }
+      __syncthreads();
+    }
+    const int rp = PH::rp(ph), lo = PH::lo(ph);
+    const int tb = (1 << K) | PH::ins_t(ph, t);
+#pragma unroll
+    for (int l = 0; l < rp; ++l) {
+      const int jb = rp - 1 - l;
+      const int bbit = lo + jb;
+      const int tsh = tb >> (bbit + 1);
+#pragma unroll
+      for (int s0 = 0; s0 < R; ++s0) {
+        if ((s0 >> jb) & 1) continue;
+        const int s1 = s0 + (1 << jb);
+        const Tw tw = args.twf[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+        fld.fwd_a(xa[s0], xa[s1], tw);
+        fld.fwd_b(xb[s0], xb[s1], tw);
+      }
+    }
+  }
+  const int rb = PH::ins_t(NPH - 1, t);
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int64_t ad = base + (int64_t)(rb + PH::cslot(NPH - 1, s)) * m;
+    args.dst0[ad] = xa[s];
+    args.dst1[ad] = xb[s];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_cols_inv2: the inverse column pass with two column groups (c and c + W) per thread, sharing
+// every twiddle load and doubling the independent butterflies per level (plain operands).
+// ------------------------------------------------------------------------------------------
+template <class F, int K, int R, int W, int MINB = 1>
+__global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
+k_cols_inv2(F fld, ColArgs<F> args) {
+  using T = typename F::T;
+  using Tw = typename F::Tw;
+  using PH = Phases<K, R>;
+  constexpr int NPH = PH::NPH;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* sma = reinterpret_cast<T*>(smem_raw);
+  T* smb = sma + (1 << K) * W;
+
+  const int c = threadIdx.x % W;
+  const int t = threadIdx.x / W;
+  const int64_t unit = blockIdx.x;
+  const int64_t inst = unit / args.colblocks;     // colblocks = m / (2 W)
+  const int64_t cb = unit - inst * args.colblocks;
+  const int64_t base = inst * args.n + cb * 2 * W + c;
+  const int64_t m = args.m;
+  auto sidx = [&](int row) { return (row ^ ((row >> PH::r) & 7)) * W + c; };
+
+  T xa[R], xb[R];
+  {
+    const int rb = PH::ins_t(NPH - 1, t);
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int64_t ad = base + (int64_t)(rb + PH::cslot(NPH - 1, s)) * m;
+      xa[s] = args.src0[ad];
+      xb[s] = args.src0[ad + W];
+    }
+  }
+#pragma unroll
+  for (int ph = NPH - 1; ph >= 0; --ph) {
+    if (ph < NPH - 1) {
+      const int wb = PH::ins_t(ph + 1, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int ad = sidx(wb + PH::cslot(ph + 1, s));
+        sma[ad] = xa[s];
+        smb[ad] = xb[s];
+      }
+      __syncthreads();
+      const int rb = PH::ins_t(ph, t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        const int ad = sidx(rb + PH::cslot(ph, s));
+        xa[s] = sma[ad];
+        xb[s] = smb[ad];
+      }
+      __syncthreads();
+    }
+    const int rp = PH::rp(ph), lo = PH::lo(ph);
+    const int tb = (1 << K) | PH::ins_t(ph, t);
+#pragma unroll
+    for (int l = 0; l < rp; ++l) {
+      const int jb = l;
+      const int bbit = lo + jb;
+      const int tsh = tb >> (bbit + 1);
+#pragma unroll
+      for (int s0 = 0; s0 < R; ++s0) {
+        if ((s0 >> jb) & 1) continue;
+        const int s1 = s0 + (1 << jb);
+        if (bbit == K - 1) {
+          fld.inv_last(xa[s0], xa[s1], args.last_si, args.last_k);
+          fld.inv_last(xb[s0], xb[s1], args.last_si, args.last_k);
+        } else {
+          const Tw tw = args.twi[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
+          fld.inv(xa[s0], xa[s1], tw);
+          fld.inv(xb[s0], xb[s1], tw);
+        }
+      }
+    }
+  }
+  const int rb = PH::ins_t(0, t);
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int64_t ad = base + (int64_t)(rb + PH::cslot(0, s)) * m;
+    args.dst0[ad] = xa[s];
+    args.dst0[ad + W] = xb[s];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // k_cols_tma: persistent, TMA-pipelined version of k_cols for plain [batch][n] operands.
 //
 // Each CTA loops over column tiles (W consecutive columns x all 2^K rows of one instance, one of

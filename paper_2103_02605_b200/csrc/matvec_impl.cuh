@@ -26,7 +26,8 @@ template <> struct FTraits<FieldU32> {
   static constexpr const char* RB = "U32_RB";
   static constexpr const char* RC = "U32_RC";
   static constexpr const char* MS = "U32_MSPLIT";
-  static constexpr int TMA_MIN_K = 5;   // TMA column passes from this depth on (profiles/r01e)
+  static constexpr int TMA_MIN_K = 9;   // TMA inverse column passes from this depth on; below it
+                                        // k_cols_inv2 measured faster (profiles/r01e_sweep_inv2.txt)
 };
 template <> struct FTraits<FieldGold> {
   static constexpr int MMAX = 13;   // 2 x 2^13 x 8 B = 128 KB smem per sub-problem
@@ -34,7 +35,7 @@ template <> struct FTraits<FieldGold> {
   static constexpr const char* RB = "GOLD_RB";
   static constexpr const char* RC = "GOLD_RC";
   static constexpr const char* MS = "GOLD_MSPLIT";
-  static constexpr int TMA_MIN_K = 9;   // at K = 8 the TMA pipeline measured 2 % slower than k_cols
+  static constexpr int TMA_MIN_K = 9;
 };
 constexpr int KMAX = 11;
 
@@ -98,6 +99,50 @@ static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStr
   dim3 grid((unsigned)args.units, INV ? 1 : 2);
   prof_begin(INV ? 3 : 2, st);
   kern<<<grid, threads, smem, st>>>(fld, args);
+  prof_end(st);
+  count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+// dual forward column pass (a and b per thread)
+template <class F, int K, int RR, bool EMB = false>
+static int launch_cols_fwd2(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
+  constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
+  constexpr int threads = W * ((1 << K) / R);
+  using E = typename F::T;
+  const size_t smem = (size_t)2 * (1 << K) * W * sizeof(E);
+  constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
+  auto kern = k_cols_fwd2<F, K, R, W, MINB, EMB>;
+  static const bool attr_ok =
+      smem <= 48 * 1024 ||
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+  if (!attr_ok) return FCIRC_ECUDA;
+  args.colblocks = args.m / W;
+  args.units = instances * args.colblocks;
+  prof_begin(2, st);
+  kern<<<(unsigned)args.units, threads, smem, st>>>(fld, args);
+  prof_end(st);
+  count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+// inverse column pass, two column groups per thread (plain operands; needs m >= 2 W)
+template <class F, int K, int RR>
+static int launch_cols_inv2(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
+  constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
+  constexpr int threads = W * ((1 << K) / R);
+  using E = typename F::T;
+  const size_t smem = (size_t)2 * (1 << K) * W * sizeof(E);
+  constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
+  auto kern = k_cols_inv2<F, K, R, W, MINB>;
+  static const bool attr_ok =
+      smem <= 48 * 1024 ||
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
+  if (!attr_ok) return FCIRC_ECUDA;
+  args.colblocks = args.m / (2 * W);
+  args.units = instances * args.colblocks;
+  prof_begin(3, st);
+  kern<<<(unsigned)args.units, threads, smem, st>>>(fld, args);
   prof_end(st);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
@@ -190,25 +235,48 @@ static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t s
   return launch_block<F, M, 16>(fld, args, st);
 }
 
+// Column-pass selection (measured, profiles/r01e_sweep_cols2.txt):
+//   forward, plain, K >= 6      -> k_cols_fwd2 (a and b per thread)        FCIRC_COLS2=0 disables
+//   forward, polynomial embed   -> k_cols_fwd2<EMB>
+//   forward, limb embed         -> k_cols<EMB> (the per-limb loads favour one operand per thread)
+//   inverse, K >= TMA_MIN_K     -> k_cols_tma (persistent, TMA double-buffered)  FCIRC_TMA=0 disables
+//   inverse, 6 <= K < TMA_MIN_K -> k_cols_inv2 (two column groups per thread)   FCIRC_INV2=0 disables
+//   otherwise                   -> k_cols (R = 16, or the FCIRC_<field>_RC variant)
 template <class F, int K, bool INV>
 static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cudaStream_t st) {
-  if (args.io.mode != EMB_PLAIN) {  // application embeddings: one variant (R = 16)
-    if (INV && args.io.mode != EMB_POLY) return launch_cols<F, K, INV, 16>(fld, args, inst, st);
+  static const int use_tma = knob("TMA", 1);
+  static const int use_fwd2 = knob("COLS2", 1);
+  static const int r = knob(FTraits<F>::RC, RDefault<F>::RC);
+  using E = typename F::T;
+  const int mode = args.io.mode;
+  if constexpr (!INV && K >= 4 && K <= 10) {
+    if (use_fwd2 && mode == EMB_POLY) return launch_cols_fwd2<F, K, 16, true>(fld, args, inst, st);
+    if (use_fwd2 && mode == EMB_PLAIN && K >= 6) {
+      if (r == 8) return launch_cols_fwd2<F, K, 8>(fld, args, inst, st);
+      return launch_cols_fwd2<F, K, 16>(fld, args, inst, st);
+    }
+  }
+  if (mode != EMB_PLAIN) {  // application embeddings: one variant (R = 16)
+    if (INV && mode != EMB_POLY) return launch_cols<F, K, INV, 16>(fld, args, inst, st);
     return launch_cols<F, K, INV, 16, true>(fld, args, inst, st);
   }
-  static const int use_tma = knob("TMA", 1);
-  using E = typename F::T;
+  static const int use_inv2 = knob("INV2", 1);
+  if constexpr (INV && K >= 6 && K <= 10) {
+    // two column groups per thread below the TMA depth (and whenever FCIRC_TMA=0)
+    if (use_inv2 && (!use_tma || K < FTraits<F>::TMA_MIN_K) && args.m >= 2 * wsel<16>(K)) {
+      if (r == 8) return launch_cols_inv2<F, K, 8>(fld, args, inst, st);
+      return launch_cols_inv2<F, K, 16>(fld, args, inst, st);
+    }
+  }
   // TMA pipeline when two stages + the exchange buffer fit in shared memory
   if constexpr (K >= FTraits<F>::TMA_MIN_K && 3 * (1 << K) * wsel<16>(K) * sizeof(E) <= 200 * 1024) {
     if (use_tma) {
-      static const int r = knob(FTraits<F>::RC, RDefault<F>::RC);
       if constexpr (K <= 10)
         if (r == 8) return launch_cols_tma<F, K, INV, 8>(fld, args, inst, st);
       return launch_cols_tma<F, K, INV, 16>(fld, args, inst, st);
     }
   }
   if constexpr (K >= 6 && K <= 10) {  // K = 11 with R = 8 would need 2048 threads
-    static const int r = knob(FTraits<F>::RC, RDefault<F>::RC);
     if (r == 8) return launch_cols<F, K, INV, 8>(fld, args, inst, st);
     if constexpr (K <= 9)
       if (r == 4) return launch_cols<F, K, INV, 4>(fld, args, inst, st);
@@ -265,8 +333,9 @@ static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void
   int64_t C = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)chunk_bytes() / per_inst));
   // plain: a' lives in c, b' in the workspace; embedded inputs: a' and b' both in the workspace
   void* ws;
-  int rc = get_workspace(dev, (void*)st, (size_t)((plain ? 1 : 2) * C * n) * sizeof(E), &ws);
+  int rc = ws_alloc(dev, st, (size_t)((plain ? 1 : 2) * C * n) * sizeof(E), &ws);
   if (rc) return rc;
+  struct Free { void* p; cudaStream_t s; ~Free() { ws_free(p, s); } } free_ws{ws, st};
   // instance strides of the caller's arrays (elements of E; 32-bit words for EMB_LIMBS)
   const int64_t sa = plain ? n : io.na, sb = plain ? n : io.nb, sc = io.mode == EMB_POLY ? io.nc : n;
   for (int64_t i0 = 0; i0 < batch; i0 += C) {

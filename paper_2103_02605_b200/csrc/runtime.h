@@ -27,8 +27,9 @@ void prof_begin(int kind, cudaStream_t st);
 void prof_end(cudaStream_t st);
 void count_launch();
 
-// grow-only device scratch per (device, stream, tag) (api.cu)
-int get_workspace(int dev, void* stream, size_t bytes, void** out, int tag = 0);
+// stream-ordered device scratch from the default memory pool (api.cu); free with ws_free on the same stream
+int ws_alloc(int dev, cudaStream_t st, size_t bytes, void** out);
+void ws_free(void* p, cudaStream_t st);
 
 // integer tuning knob read once from the environment (FCIRC_<name>), else `dflt`
 int knob(const char* name, int dflt);
