@@ -812,6 +812,7 @@ struct FieldGoldG5 {  // experiment: forward = G4, inverse = current mask arithm
   }
 };
 
+
 struct FieldGoldG6 {  // experiment: forward = G4, inverse = mask add + select canonicalisation
   using T = uint64_t;
   using Tw = uint64_t;
