@@ -75,6 +75,22 @@ int fcirc_matvec(uint64_t p, uint64_t f, const void* a, const void* b, void* c,
                  int64_t n, int64_t batch, void* stream);
 
 /*
+ * fcirc_circulant_matvec — c = A b for a batch of usual circulant matrices (f = 1) of
+ * ANY order n >= 1 (Corollary 1).  A is identified by its first row a:
+ *     c_i = sum_j a[(j - i) mod n] b_j   (mod p).
+ * n a power of two: exactly fcirc_matvec with f = 1.  Otherwise the Corollary's embedding: the
+ * order-N circulant with row a' = (a_0..a_{n-1}, 0..0, a_1..a_{n-1}) times b' = (b, 0..0), whose
+ * first n entries are A b; N = the smallest power of two >= 2n - 1 (the paper's N = 2^{d+1} with
+ * 2^d > n also works, at up to twice the size; reading R10).  The embedding is fused into
+ * the first pass's loads and the truncation into the last pass's stores.
+ *   p, a, b, c, batch, stream as fcirc_matvec; a, b, c are [batch][n]; N must divide p-1 and be
+ *   within the fcirc_matvec maximum.
+ * Errors: FCIRC_EINVAL, FCIRC_EPRIME, FCIRC_ESIZE, FCIRC_ENOMEM, FCIRC_ECUDA.
+ */
+int fcirc_circulant_matvec(uint64_t p, const void* a, const void* b, void* c, int64_t n, int64_t batch,
+                           void* stream);
+
+/*
  * fcirc_matvec_host — fcirc_matvec on HOST buffers: copies a, b to the device, runs the product
  * and copies c back, pipelined in chunks of instances over two streams so the PCIe transfers in
  * both directions overlap the kernels.  Synchronous: returns when c is written.  Same arguments

@@ -7,6 +7,7 @@ device memory and streams.  There is no CPU fallback: if the library is missing 
 Functions mirror the C ABI names:
   matvec(a, b, f, p, out=None)      -> fcirc_matvec       (device tensors [batch, n])
   matvec_host(a, b, f, p, out=None) -> fcirc_matvec_host  (host arrays/tensors, pinned preferred)
+  circulant_matvec(a, b, p)         -> fcirc_circulant_matvec (f = 1, any order n: Corollary 1)
   polymul(a, b, p, out=None)        -> fcirc_polymul      (device tensors [batch, na], [batch, nb])
   bigint_mul(x, y, out=None)        -> bigint_mul         (device uint32 words [batch, nx], [batch, ny])
   plan_table(p, f, n)               -> fcirc_plan_table   (host-only twist-table inspection)
@@ -18,7 +19,7 @@ import os
 
 import numpy as np
 
-__all__ = ["FcircError", "matvec", "matvec_host", "polymul", "bigint_mul", "plan_table", "strerror",
+__all__ = ["FcircError", "matvec", "matvec_host", "circulant_matvec", "polymul", "bigint_mul", "plan_table", "strerror",
            "last_launch_count", "release_cache", "version", "library_path", "schedule", "P998", "P469", "P167",
            "GOLDILOCKS", "PRIMES"]
 
@@ -54,13 +55,14 @@ def _load():
     u64, i64, vp = ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p
     lib.fcirc_matvec.argtypes = [u64, u64, vp, vp, vp, i64, i64, vp]
     lib.fcirc_matvec_host.argtypes = [u64, u64, vp, vp, vp, i64, i64]
+    lib.fcirc_circulant_matvec.argtypes = [u64, vp, vp, vp, i64, i64, vp]
     lib.fcirc_polymul.argtypes = [u64, vp, i64, vp, i64, vp, i64, vp]
     lib.bigint_mul.argtypes = [vp, i64, vp, i64, vp, i64, vp]
     lib.fcirc_plan_table.argtypes = [u64, u64, i64, vp, vp, ctypes.POINTER(u64), ctypes.POINTER(u64)]
     lib.fcirc_schedule.argtypes = [u64, i64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
     lib.fcirc_profile_enable.argtypes = [ctypes.c_int]
     lib.fcirc_profile_read.argtypes = [vp, vp, ctypes.c_int]
-    for fn in (lib.fcirc_matvec, lib.fcirc_matvec_host, lib.fcirc_polymul, lib.bigint_mul, lib.fcirc_plan_table,
+    for fn in (lib.fcirc_matvec, lib.fcirc_matvec_host, lib.fcirc_circulant_matvec, lib.fcirc_polymul, lib.bigint_mul, lib.fcirc_plan_table,
                lib.fcirc_schedule,
                lib.fcirc_release_cache, lib.fcirc_profile_enable, lib.fcirc_profile_read):
         fn.restype = ctypes.c_int
@@ -157,6 +159,27 @@ def matvec(a, b, f: int, p: int, out=None, stream=None):
     rc = _load().fcirc_matvec(int(p), int(f) % int(p), a.data_ptr(), b.data_ptr(), out.data_ptr(), n, batch,
                               _stream_handle(stream))
     _check(rc, "fcirc_matvec")
+    return out
+
+
+def circulant_matvec(a, b, p: int, out=None, stream=None):
+    """c = A b for usual circulants (f = 1) of ANY order n (Corollary 1), batched.
+
+    ``a``, ``b``: CUDA tensors [batch, n] of residues (element type as in ``matvec``).
+    """
+    torch = _torch()
+    _dev_tensor(a, p, "a")
+    _dev_tensor(b, p, "b")
+    if a.shape != b.shape:
+        raise ValueError("a and b must have the same shape")
+    n = a.shape[-1]
+    batch = a.numel() // n if n else 0
+    if out is None:
+        out = torch.empty_like(a)
+    _dev_tensor(out, p, "out")
+    rc = _load().fcirc_circulant_matvec(int(p), a.data_ptr(), b.data_ptr(), out.data_ptr(), n, batch,
+                                        _stream_handle(stream))
+    _check(rc, "fcirc_circulant_matvec")
     return out
 
 

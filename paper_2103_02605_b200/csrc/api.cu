@@ -440,6 +440,32 @@ int fcirc_matvec(uint64_t p, uint64_t f, const void* a, const void* b, void* c, 
   return matvec_impl(p, f, a, b, c, n, batch, (cudaStream_t)stream);
 }
 
+int fcirc_circulant_matvec(uint64_t p, const void* a, const void* b, void* c, int64_t n, int64_t batch,
+                           void* stream) {
+  g_launches = 0;
+  if (!a || !b || !c || n < 1 || batch < 1) return FCIRC_EINVAL;
+  const PrimeInfo* pi = prime_info(p);
+  if (!pi) return FCIRC_EPRIME;
+  const size_t es = pi->wide ? 8 : 4;
+  const size_t bytes = (size_t)n * (size_t)batch * es;
+  if (overlaps(c, bytes, a, bytes) || overlaps(c, bytes, b, bytes)) return FCIRC_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = check_canonical(p, pi->wide, a, n * batch, st);
+  if (rc == FCIRC_OK) rc = check_canonical(p, pi->wide, b, n * batch, st);
+  if (rc) return rc;
+  if ((n & (n - 1)) == 0) return matvec_core(p, 1, a, b, c, ilog2_exact(n), batch, st, EmbedIO{});
+  // Corollary 1: order N = the smallest power of two >= 2n - 1 (reading R10)
+  const int64_t N = next_pow2(2 * n - 1);
+  const int LN = ilog2_exact(N);
+  if (LN > pi->two_adicity || LN > max_log_n(pi->wide)) return FCIRC_ESIZE;
+  EmbedIO io;
+  io.mode = EMB_ANYN;
+  io.na = n;
+  io.nb = n;
+  io.nc = n;
+  return matvec_core(p, 1, a, b, c, LN, batch, st, io);
+}
+
 int fcirc_matvec_host(uint64_t p, uint64_t f, const void* a, const void* b, void* c, int64_t n,
                       int64_t batch) {
   g_launches = 0;

@@ -79,8 +79,12 @@ __host__ __device__ __forceinline__ constexpr int swz(int x) {
 //               vector b zero-padded; c truncated to nc = na + nb - 1 coefficients.
 //   EMB_LIMBS   big integers: a, b are [batch][na | nb] little-endian 32-bit words read
 //               as 16-bit limbs (row = reversed limbs of a, vector = limbs of b); c is [batch][n].
+//   EMB_ANYN    Corollary 1: a circulant of any order na (= nb = nc) embedded in one of
+//               order n (a power of two >= 2 na - 1): row a' = (a_0..a_{na-1}, 0..0, a_1..a_{na-1}),
+//               vector b' = (b, 0..0); c = the first na entries of A' b'.
 // ------------------------------------------------------------------------------------------
-enum { EMB_PLAIN = 0, EMB_POLY = 1, EMB_LIMBS = 2 };
+enum { EMB_PLAIN = 0, EMB_POLY = 1, EMB_LIMBS = 2, EMB_ANYN = 3 };
+__host__ __device__ __forceinline__ bool emb_truncates(int mode) { return mode == EMB_POLY || mode == EMB_ANYN; }
 struct EmbedIO {
   int mode = EMB_PLAIN;
   int64_t na = 0, nb = 0;   // EMB_POLY: coefficients per instance; EMB_LIMBS: 32-bit words
@@ -101,13 +105,18 @@ __device__ __forceinline__ T io_load(const T* src, int64_t inst, int64_t pos, in
     const T* ai = src + inst * io.na;
     return pos == 0 ? ai[0] : (pos > n - io.na ? ai[n - pos] : (T)0);
   }
+  if (io.mode == EMB_ANYN) {
+    if (second) return pos < io.nb ? src[inst * io.nb + pos] : (T)0;
+    const T* ai = src + inst * io.na;
+    return pos < io.na ? ai[pos] : (pos > n - io.na ? ai[pos - (n - io.na)] : (T)0);
+  }
   if (second) return pos < 2 * io.nb ? limb_at(src + inst * io.nb, pos) : (T)0;
   const T* xi = src + inst * io.na;
   return pos == 0 ? limb_at(xi, 0) : (pos > n - 2 * io.na ? limb_at(xi, n - pos) : (T)0);
 }
 template <class T>
 __device__ __forceinline__ void io_store(T* dst, int64_t inst, int64_t pos, int64_t n, T v, const EmbedIO& io) {
-  if (io.mode == EMB_POLY) {
+  if (emb_truncates(io.mode)) {
     if (pos < io.nc) dst[inst * io.nc + pos] = v;
   } else {
     dst[inst * n + pos] = v;
@@ -298,7 +307,7 @@ k_block(F fld, BlockArgs<F> args) {
   }
 
   // ---- store (phase-0 addresses, coalesced)
-  if (active && (!EMB || args.io.mode != EMB_POLY)) {
+  if (active && (!EMB || !emb_truncates(args.io.mode))) {
 #pragma unroll
     for (int s = 0; s < R; ++s) args.out[base + PH::ins_t(0, t) + PH::cslot(0, s)] = xm[s];
   } else if (active) {
@@ -436,7 +445,7 @@ k_cols(F fld, ColArgs<F> args) {
       }
     }
     const int rb = PH::ins_t(0, t);
-    if (!EMB || args.io.mode != EMB_POLY) {
+    if (!EMB || !emb_truncates(args.io.mode)) {
 #pragma unroll
       for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(0, s)) * m] = x[s];
     } else {

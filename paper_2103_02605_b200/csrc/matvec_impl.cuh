@@ -237,7 +237,7 @@ static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t s
 
 // Column-pass selection (measured, profiles/r01e_sweep_cols2.txt):
 //   forward, plain, K >= 6      -> k_cols_fwd2 (a and b per thread)        FCIRC_COLS2=0 disables
-//   forward, polynomial embed   -> k_cols_fwd2<EMB>
+//   forward, polynomial / any-n -> k_cols_fwd2<EMB>
 //   forward, limb embed         -> k_cols<EMB> (the per-limb loads favour one operand per thread)
 //   inverse, K >= TMA_MIN_K     -> k_cols_tma (persistent, TMA double-buffered)  FCIRC_TMA=0 disables
 //   inverse, 6 <= K < TMA_MIN_K -> k_cols_inv2 (two column groups per thread)   FCIRC_INV2=0 disables
@@ -250,14 +250,14 @@ static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cud
   using E = typename F::T;
   const int mode = args.io.mode;
   if constexpr (!INV && K >= 4 && K <= 10) {
-    if (use_fwd2 && mode == EMB_POLY) return launch_cols_fwd2<F, K, 16, true>(fld, args, inst, st);
+    if (use_fwd2 && (mode == EMB_POLY || mode == EMB_ANYN)) return launch_cols_fwd2<F, K, 16, true>(fld, args, inst, st);
     if (use_fwd2 && mode == EMB_PLAIN && K >= 6) {
       if (r == 8) return launch_cols_fwd2<F, K, 8>(fld, args, inst, st);
       return launch_cols_fwd2<F, K, 16>(fld, args, inst, st);
     }
   }
   if (mode != EMB_PLAIN) {  // application embeddings: one variant (R = 16)
-    if (INV && mode != EMB_POLY) return launch_cols<F, K, INV, 16>(fld, args, inst, st);
+    if (INV && !emb_truncates(mode)) return launch_cols<F, K, INV, 16>(fld, args, inst, st);
     return launch_cols<F, K, INV, 16, true>(fld, args, inst, st);
   }
   static const int use_inv2 = knob("INV2", 1);
@@ -337,7 +337,7 @@ static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void
   if (rc) return rc;
   struct Free { void* p; cudaStream_t s; ~Free() { ws_free(p, s); } } free_ws{ws, st};
   // instance strides of the caller's arrays (elements of E; 32-bit words for EMB_LIMBS)
-  const int64_t sa = plain ? n : io.na, sb = plain ? n : io.nb, sc = io.mode == EMB_POLY ? io.nc : n;
+  const int64_t sa = plain ? n : io.na, sb = plain ? n : io.nb, sc = emb_truncates(io.mode) ? io.nc : n;
   for (int64_t i0 = 0; i0 < batch; i0 += C) {
     const int64_t cc = std::min<int64_t>(C, batch - i0);
     const E* ai = (const E*)a + i0 * sa;

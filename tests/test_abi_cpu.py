@@ -172,3 +172,12 @@ def test_schedule_host_only():
         fc.schedule(P998, 12)
     with pytest.raises(fc.FcircError):
         fc.schedule(12345, 16)
+
+
+def test_circulant_any_n_validation_before_device():
+    lib = fc._load()
+    assert lib.fcirc_circulant_matvec(P998, 1, 2, 3, 0, 1, None) == -1        # n < 1
+    assert lib.fcirc_circulant_matvec(P998, 1, 2, 3, 5, 0, None) == -1        # batch < 1
+    assert lib.fcirc_circulant_matvec(P998, 0, 2, 3, 5, 1, None) == -1        # null
+    assert lib.fcirc_circulant_matvec(1000003, 1, 2, 3, 5, 1, None) == -2     # p not in the registry
+    assert lib.fcirc_circulant_matvec(P998, 8, 8, 8, 5, 4, None) == -1        # c overlaps a

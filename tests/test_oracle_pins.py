@@ -352,3 +352,30 @@ def test_eigen_check_detects_a_single_corrupted_entry():
     assert oracle.eigen_check(p, n, f, a, b, c, th)
     c[17] = (c[17] + 1) % p
     assert not oracle.eigen_check(p, n, f, a, b, c, th)
+
+
+def test_corollary1_embedding_any_n():
+    """Corollary 1: for non-power-of-two n, the order-N circulant with row
+    a' = (a_1..a_n, 0..0, a_2..a_n) times b' = (b, 0..0) has A b as its first n entries -- with the
+    paper's N = 2^{d+1} (2^d the smallest power of two > n) and with the smallest power of two
+    N >= 2n - 1 that libfcirc uses (reading R10).  Oracle = Definition 2 at both orders."""
+    import oracle
+    rng = random.Random(102)
+    p = P998
+    for n in list(range(1, 41)) + [63, 65, 100]:
+        a = [rng.randrange(p) for _ in range(n)]
+        b = [rng.randrange(p) for _ in range(n)]
+        ref = [int(v) for v in oracle.fcirc_entries(p, 1, a, b)]
+        d = 0
+        while (1 << d) <= n:
+            d += 1
+        paper_N = 1 << (d + 1)
+        min_N = 1
+        while min_N < 2 * n - 1:
+            min_N <<= 1
+        for N in {paper_N, min_N}:
+            a2 = a + [0] * (N - 2 * n + 1) + a[1:]
+            b2 = b + [0] * (N - n)
+            assert len(a2) == N and len(b2) == N
+            got = [int(v) for v in oracle.fcirc_entries(p, 1, a2, b2)][:n]
+            assert got == ref, (n, N)

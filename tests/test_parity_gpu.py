@@ -364,3 +364,16 @@ except fc.FcircError as e:
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                          cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert "rejected -1" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("p", [P998, GOLDILOCKS])
+def test_circulant_any_n_corollary1(p):
+    """fcirc_circulant_matvec (Corollary 1): usual circulant of any order n, every entry
+    against Definition 2 with f = 1 -- fused (N <= 2^12) and multi-pass embeddings, powers of two."""
+    for n, batch in [(1, 3), (3, 2), (5, 2), (7, 3), (100, 2), (1000, 2), (1024, 2), (3000, 2), (5000, 1),
+                     (40000, 1)]:
+        inp = synth.matvec_inputs(p, n, batch, seed=400 + n, f_mode="one")
+        c = _host(fc.circulant_matvec(_dev(inp["a"]), _dev(inp["b"]), p))
+        for k in range(batch):
+            exp = oracle.fcirc_entries(p, 1, inp["a"][k], inp["b"][k])
+            assert np.array_equal(c[k].astype(np.uint64), exp), (n, k)
