@@ -226,7 +226,7 @@ template <class F, int M>
 static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
   // the application embeddings (fused path only) use one variant: the default R
   if (args.k == 0 && args.io.mode != EMB_PLAIN) return launch_block<F, M, RDefault<F>::RB, true>(fld, args, st);
-  if constexpr (M >= FTraits<F>::MMAX - 1) {
+  if constexpr (M >= FTraits<F>::MMAX - 2) {
     static const int r = knob(FTraits<F>::RB, RDefault<F>::RB);
     if (r == 8) return launch_block<F, M, 8>(fld, args, st);
     if constexpr ((1 << M) / 4 <= 1024)  // one sub-problem per CTA: at most 1024 threads
@@ -300,13 +300,14 @@ static int dispatch_cols(int K, const F& fld, const ColArgs<F>& args, int64_t in
   return rc;
 }
 
-// On-chip sub-problem size for a product of order 2^L: the preferred split (FCIRC_<field>_MSPLIT,
-// default FTraits::MPREF; u32 prefers 2^12 = two CTAs per SM over 2^13 = one, profiles/r01d), grown
+// On-chip sub-problem size for a product of order 2^L: the preferred split (FCIRC_<field>_MSPLIT in
+// [MMAX-2, MMAX], default FTraits::MPREF; u32 prefers 2^12 = two CTAs per SM over 2^13 = one,
+// profiles/r01d), grown
 // up to MMAX only when the column passes would need more than KMAX levels.
 template <class F>
 static int msplit(int L) {
   static const int pref = std::min(FTraits<F>::MMAX,
-                                   std::max(FTraits<F>::MMAX - 1, knob(FTraits<F>::MS, FTraits<F>::MPREF)));
+                                   std::max(FTraits<F>::MMAX - 2, knob(FTraits<F>::MS, FTraits<F>::MPREF)));
   return std::min(FTraits<F>::MMAX, std::max(pref, L - KMAX));
 }
 
