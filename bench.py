@@ -60,6 +60,8 @@ WORKLOADS = {
        for L in range(12, 23) if L != 20},
     "C3": "C3: polynomial products mod 998244353, 2^20 x 2^20 coefficients -> 2^21 circulant (f=1), batch 16",
     "C5": "C5: 2^22-bit integer products, 16-bit limbs, 3 primes x 2^19 circulant (f=1) + CRT + carry, batch 8",
+    **{f"S2_n{n}": (f"S2 (context): the paper's experiment, 10000 products of two {n}-coefficient polynomials in "
+                    f"Z/(2^31-1)[sqrt 3] (P:110-133)") for n in (8, 16, 32, 64, 128, 256, 512)},
 }
 
 
@@ -196,7 +198,7 @@ def algorithmic_modmuls(kind: str, n: int, batch: int, M: int, K: int) -> float:
 
 
 def cfg_dtype(p: int) -> str:
-    return "u64" if p >= (1 << 32) else "u32"
+    return "u64" if p >= (1 << 32) or p == synth.M31X2 else "u32"
 
 
 def next_pow2(x: int) -> int:
@@ -310,9 +312,16 @@ class Workload:
                     f"{reps} full products of instance {k} (independent Karatsuba on 32-bit words, "
                     f"one thread); counted as {self.n} output limb positions each")
         if self.kind == "polymul":
-            fn = lambda ks: oracle.polymul_coeffs(self.p, i["a"][k], i["b"][k], ks)  # noqa: E731
+            if self.p == synth.M31X2:
+                fn = lambda ks: oracle.polymul_coeffs_m31x2(i["a"][k], i["b"][k], ks)  # noqa: E731
+            else:
+                fn = lambda ks: oracle.polymul_coeffs(self.p, i["a"][k], i["b"][k], ks)  # noqa: E731
             what = "schoolbook coefficients"
             total = i["na"] + i["nb"] - 1
+        elif self.p == synth.M31X2:
+            fn = lambda ks: oracle.fcirc_entries_m31x2(self.inp["f"], i["a"][k], i["b"][k], ks)  # noqa: E731
+            what = "output entries (Definition 2 over Z/(2^31-1)[sqrt 3])"
+            total = self.n
         else:
             fn = lambda ks: oracle.fcirc_entries(self.p, self.inp["f"], i["a"][k], i["b"][k], ks)  # noqa: E731
             what = "output entries (Definition 2, O(n) multiply-adds each)"
@@ -505,6 +514,8 @@ def run_fcirc(args):
             "gpu_launches": launches, "clocks": sampler.summary(), "plan_build_ms": plan_ms,
             "timing": "CUDA graph replay of the step" if use_graph else "API call per step",
         }
+        if wl.kind in ("polymul", "bigint"):
+            line["products_per_s"] = world * wl.batch * args.steps / (ms_max * 1e-3)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -11,6 +11,9 @@
  *        469762049  =   7*2^26 + 1   (uint32_t)
  *        167772161  =   5*2^25 + 1   (uint32_t)
  *        18446744069414584321 = 2^64 - 2^32 + 1  "Goldilocks"  (uint64_t)
+ *        2147483647 = 2^31 - 1 selects the paper's own ring Z/pZ[sqrt 3] (3 is a non-residue):
+ *          an element u + v sqrt 3 (u, v < p) is a uint64_t packed as u | v << 32, and so is f;
+ *          roots of unity are the paper's (2 + sqrt 3)^((p+1)/N); n <= 2^24
  *    The element type of a, b, c follows p: uint32_t for the three 32-bit primes, uint64_t for
  *    Goldilocks.  Inputs must be canonical residues in [0, p) (precondition, not checked on the
  *    device unless the environment sets FCIRC_CHECK_INPUTS=1: then fcirc_matvec / fcirc_polymul

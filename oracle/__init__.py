@@ -58,6 +58,10 @@ def _load():
                                          ctypes.c_int]
         lib.oracle_poly_eval.restype = ctypes.c_int
         lib.oracle_bigint_mul.argtypes = [u32p, ctypes.c_int64, u32p, ctypes.c_int64, u32p]
+        lib.oracle_fcirc_entries_m31x2.argtypes = [ctypes.c_uint64, u64p, u64p, ctypes.c_int64, i64p, ctypes.c_int64,
+                                                   u64p, ctypes.c_int]
+        lib.oracle_polymul_coeffs_m31x2.argtypes = [u64p, ctypes.c_int64, u64p, ctypes.c_int64, i64p, ctypes.c_int64,
+                                                    u64p, ctypes.c_int]
         lib.oracle_bigint_mul_school.argtypes = [u32p, ctypes.c_int64, u32p, ctypes.c_int64, u32p]
         for fn in (lib.oracle_fcirc_entries, lib.oracle_polymul_coeffs, lib.oracle_bigint_mul,
                    lib.oracle_bigint_mul_school):
@@ -112,6 +116,75 @@ def polymul_coeffs(p: int, a, b, ks=None, threads: int | None = None) -> np.ndar
                                    threads or default_threads())
     if rc != 0:
         raise ValueError("oracle_polymul_coeffs: bad arguments")
+    return out
+
+
+# ---------------------------------------------------------------- the paper's ring
+M31 = (1 << 31) - 1   # Z/pZ[sqrt 3]: u + v sqrt 3 packed as u | v << 32
+
+
+def fcirc_entries_m31x2(f: int, a, b, idx=None, threads: int | None = None) -> np.ndarray:
+    """Definition 2 over Z/(2^31-1)[sqrt 3]; a, b, f packed u | v << 32."""
+    lib = _load()
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.uint64))
+    n = a.shape[0]
+    idx = np.arange(n, dtype=np.int64) if idx is None else np.ascontiguousarray(np.asarray(idx, dtype=np.int64))
+    out = np.zeros(idx.shape[0], dtype=np.uint64)
+    rc = lib.oracle_fcirc_entries_m31x2(int(f), _ptr(a, ctypes.c_uint64), _ptr(b, ctypes.c_uint64), n,
+                                        _ptr(idx, ctypes.c_int64), idx.shape[0], _ptr(out, ctypes.c_uint64),
+                                        threads or default_threads())
+    if rc != 0:
+        raise ValueError("oracle_fcirc_entries_m31x2: bad arguments")
+    return out
+
+
+def polymul_coeffs_m31x2(a, b, ks=None, threads: int | None = None) -> np.ndarray:
+    """Schoolbook product coefficients over Z/(2^31-1)[sqrt 3] (the paper's experiment)."""
+    lib = _load()
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.uint64))
+    na, nb = a.shape[0], b.shape[0]
+    ks = (np.arange(na + nb - 1, dtype=np.int64) if ks is None
+          else np.ascontiguousarray(np.asarray(ks, dtype=np.int64)))
+    out = np.zeros(ks.shape[0], dtype=np.uint64)
+    rc = lib.oracle_polymul_coeffs_m31x2(_ptr(a, ctypes.c_uint64), na, _ptr(b, ctypes.c_uint64), nb,
+                                         _ptr(ks, ctypes.c_int64), ks.shape[0], _ptr(out, ctypes.c_uint64),
+                                         threads or default_threads())
+    if rc != 0:
+        raise ValueError("oracle_polymul_coeffs_m31x2: bad arguments")
+    return out
+
+
+def py_fp2_mul(x: int, y: int) -> int:
+    """Python-int product in Z/(2^31-1)[sqrt 3] on packed elements (second witness, no tricks)."""
+    u1, v1, u2, v2 = x & 0xFFFFFFFF, x >> 32, y & 0xFFFFFFFF, y >> 32
+    return ((u1 * u2 + 3 * v1 * v2) % M31) | (((u1 * v2 + u2 * v1) % M31) << 32)
+
+
+def py_fp2_pow(x: int, e: int) -> int:
+    r = 1
+    while e:
+        if e & 1:
+            r = py_fp2_mul(r, x)
+        x = py_fp2_mul(x, x)
+        e >>= 1
+    return r
+
+
+def py_fcirc_matvec_m31x2(f: int, a, b):
+    """Definition 2 over Z/(2^31-1)[sqrt 3] with Python ints, for small n (witness of the C oracle)."""
+    n = len(a)
+    out = []
+    for i in range(n):
+        acc_u = acc_v = 0
+        for j in range(n):
+            t = py_fp2_mul(int(a[(j - i) % n]), int(b[j]))
+            if j < i:
+                t = py_fp2_mul(int(f), t)
+            acc_u += t & 0xFFFFFFFF
+            acc_v += t >> 32
+        out.append((acc_u % M31) | ((acc_v % M31) << 32))
     return out
 
 

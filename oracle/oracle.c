@@ -18,6 +18,9 @@
  *                            C_k = sum_{i} a_i b_{k-i} (mod p).  O(n) per coefficient.
  *   oracle_poly_eval       sum_i c_i x^i mod p by Horner's rule (used for the eigen-checksum of
  *                          SURVEY App. B.4 and Schwartz-Zippel checks; a plain definition).
+ *   oracle_fcirc_entries_m31x2, oracle_polymul_coeffs_m31x2
+ *                          the same definitions over the paper's own ring Z/pZ[sqrt 3],
+ *                          p = 2^31 - 1, elements packed u | v << 32.
  *   oracle_bigint_mul      product of two non-negative integers given as little-endian 32-bit
  *                          words (P:135-140 application): an independent Karatsuba recursion
  *                          (schoolbook below 32 words).  Exact, full product.
@@ -73,7 +76,7 @@ static uint64_t fcirc_entry(uint64_t p, uint64_t f, const uint64_t* a, const uin
 
 /* ---------------- threading helper ---------------- */
 typedef struct {
-  int kind;  /* 0 = fcirc entries, 1 = polymul coefficients */
+  int kind;  /* 0 = fcirc entries, 1 = polymul coefficients, 2/3 = the same over Z/(2^31-1)[sqrt 3] */
   uint64_t p, f;
   const uint64_t *a, *b;
   int64_t n, na, nb;
@@ -91,11 +94,50 @@ static uint64_t poly_coeff(uint64_t p, const uint64_t* a, int64_t na, const uint
   return acc_mod(&s, p);
 }
 
+/* ---------------- the paper's ring Z/pZ[sqrt 3], p = 2^31 - 1 ----------------
+ * u + v sqrt 3 packed as u | v << 32.  (u1 + v1 s)(u2 + v2 s) = (u1 u2 + 3 v1 v2) + (u1 v2 + u2 v1) s,
+ * s^2 = 3.  Sums of products are accumulated exactly per component and reduced once. */
+#define M31 2147483647ull
+static inline uint64_t cu(uint64_t x) { return x & 0xFFFFFFFFull; }
+static inline uint64_t cv(uint64_t x) { return x >> 32; }
+static inline void fp2_acc(acc192* U, acc192* V, uint64_t x, uint64_t y) {
+  acc_add(U, (u128)cu(x) * cu(y));
+  acc_add(U, (u128)3 * ((u128)cv(x) * cv(y)));
+  acc_add(V, (u128)cu(x) * cv(y));
+  acc_add(V, (u128)cv(x) * cu(y));
+}
+static uint64_t fp2_mulp(uint64_t x, uint64_t y) {
+  acc192 U = {0, 0}, V = {0, 0};
+  fp2_acc(&U, &V, x, y);
+  return acc_mod(&U, M31) | (acc_mod(&V, M31) << 32);
+}
+static uint64_t fp2_addp(uint64_t x, uint64_t y) {
+  return ((cu(x) + cu(y)) % M31) | (((cv(x) + cv(y)) % M31) << 32);
+}
+/* c_i of Definition 2 over Z/pZ[sqrt 3] */
+static uint64_t fcirc_entry_m31x2(uint64_t f, const uint64_t* a, const uint64_t* b, int64_t n, int64_t i) {
+  acc192 Uu = {0, 0}, Uv = {0, 0}, Wu = {0, 0}, Wv = {0, 0};
+  for (int64_t j = i; j < n; ++j) fp2_acc(&Uu, &Uv, a[j - i], b[j]);
+  for (int64_t j = 0; j < i; ++j) fp2_acc(&Wu, &Wv, a[n + j - i], b[j]);
+  const uint64_t up = acc_mod(&Uu, M31) | (acc_mod(&Uv, M31) << 32);
+  const uint64_t wr = acc_mod(&Wu, M31) | (acc_mod(&Wv, M31) << 32);
+  return fp2_addp(up, fp2_mulp(f, wr));
+}
+static uint64_t poly_coeff_m31x2(const uint64_t* a, int64_t na, const uint64_t* b, int64_t nb, int64_t k) {
+  acc192 U = {0, 0}, V = {0, 0};
+  int64_t i0 = k - (nb - 1); if (i0 < 0) i0 = 0;
+  int64_t i1 = k; if (i1 > na - 1) i1 = na - 1;
+  for (int64_t i = i0; i <= i1; ++i) fp2_acc(&U, &V, a[i], b[k - i]);
+  return acc_mod(&U, M31) | (acc_mod(&V, M31) << 32);
+}
+
 static void* worker(void* arg) {
   job_t* J = (job_t*)arg;
   for (int64_t t = J->lo; t < J->hi; ++t) {
     if (J->kind == 0) J->out[t] = fcirc_entry(J->p, J->f, J->a, J->b, J->n, J->idx[t]);
-    else J->out[t] = poly_coeff(J->p, J->a, J->na, J->b, J->nb, J->idx[t]);
+    else if (J->kind == 1) J->out[t] = poly_coeff(J->p, J->a, J->na, J->b, J->nb, J->idx[t]);
+    else if (J->kind == 2) J->out[t] = fcirc_entry_m31x2(J->f, J->a, J->b, J->n, J->idx[t]);
+    else J->out[t] = poly_coeff_m31x2(J->a, J->na, J->b, J->nb, J->idx[t]);
   }
   return NULL;
 }
@@ -268,4 +310,24 @@ int oracle_bigint_mul_school(const uint32_t* x, int64_t nx, const uint32_t* y, i
   if (!x || !y || !z || nx < 1 || ny < 1) return -1;
   school(x, nx, y, ny, z);
   return 0;
+}
+
+/*
+ * The same two definitions over the paper's ring Z/pZ[sqrt 3], p = 2^31 - 1: elements and f
+ * packed u | v << 32 with u, v < p.  Returns 0, or -1 on bad arguments.
+ */
+int oracle_fcirc_entries_m31x2(uint64_t f, const uint64_t* a, const uint64_t* b, int64_t n, const int64_t* idx,
+                               int64_t nidx, uint64_t* out, int threads) {
+  if (!a || !b || !idx || !out || n < 1 || nidx < 0) return -1;
+  for (int64_t t = 0; t < nidx; ++t) if (idx[t] < 0 || idx[t] >= n) return -1;
+  job_t J = {2, M31, f, a, b, n, 0, 0, idx, out, 0, 0};
+  return run_jobs(J, nidx, threads);
+}
+
+int oracle_polymul_coeffs_m31x2(const uint64_t* a, int64_t na, const uint64_t* b, int64_t nb, const int64_t* ks,
+                                int64_t nk, uint64_t* out, int threads) {
+  if (!a || !b || !ks || !out || na < 1 || nb < 1 || nk < 0) return -1;
+  for (int64_t t = 0; t < nk; ++t) if (ks[t] < 0 || ks[t] > na + nb - 2) return -1;
+  job_t J = {3, M31, 0, a, b, 0, na, nb, ks, out, 0, 0};
+  return run_jobs(J, nk, threads);
 }

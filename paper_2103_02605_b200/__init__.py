@@ -21,13 +21,21 @@ import numpy as np
 
 __all__ = ["FcircError", "matvec", "matvec_host", "circulant_matvec", "polymul", "bigint_mul", "plan_table", "strerror",
            "last_launch_count", "release_cache", "version", "library_path", "schedule", "P998", "P469", "P167",
-           "GOLDILOCKS", "PRIMES"]
+           "GOLDILOCKS", "PRIMES", "M31X2", "fp2_pack"]
 
 P998 = 998244353
 P469 = 469762049
 P167 = 167772161
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
 PRIMES = (P998, P469, P167, GOLDILOCKS)
+# The paper's own ring Z/pZ[sqrt 3], p = 2^31 - 1: pass p = M31X2; elements u + v sqrt 3 are
+# uint64 packed u | v << 32 (fp2_pack), including the scalar f.
+M31X2 = (1 << 31) - 1
+
+
+def fp2_pack(u: int, v: int) -> int:
+    """u + v sqrt 3 in Z/(2^31 - 1)[sqrt 3] -> the packed 64-bit element (u, v canonical)."""
+    return (int(u) % M31X2) | ((int(v) % M31X2) << 32)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "lib", "libfcirc.so")
@@ -114,7 +122,12 @@ def _check(rc: int, where: str):
 
 
 def _elem_bytes(p: int) -> int:
-    return 8 if int(p) >= (1 << 32) else 4
+    return 8 if int(p) >= (1 << 32) or int(p) == M31X2 else 4
+
+
+def _scalar(f: int, p: int) -> int:
+    """f reduced mod p; packed Z/p[sqrt 3] scalars are passed as they are."""
+    return int(f) if int(p) == M31X2 else int(f) % int(p)
 
 
 def _torch():
@@ -156,7 +169,7 @@ def matvec(a, b, f: int, p: int, out=None, stream=None):
     if out is None:
         out = torch.empty_like(a)
     _dev_tensor(out, p, "out")
-    rc = _load().fcirc_matvec(int(p), int(f) % int(p), a.data_ptr(), b.data_ptr(), out.data_ptr(), n, batch,
+    rc = _load().fcirc_matvec(int(p), _scalar(f, p), a.data_ptr(), b.data_ptr(), out.data_ptr(), n, batch,
                               _stream_handle(stream))
     _check(rc, "fcirc_matvec")
     return out
@@ -207,7 +220,7 @@ def matvec_host(a, b, f: int, p: int, out=None):
     pc, sc = _host_ptr(out, p, "out")
     n = sa[-1]
     batch = int(np.prod(sa)) // n
-    rc = _load().fcirc_matvec_host(int(p), int(f) % int(p), pa, pb, pc, n, batch)
+    rc = _load().fcirc_matvec_host(int(p), _scalar(f, p), pa, pb, pc, n, batch)
     _check(rc, "fcirc_matvec_host")
     return out
 
@@ -263,7 +276,7 @@ def plan_table(p: int, f: int, n: int):
     si = np.zeros(size, dtype=np.uint64)
     w = ctypes.c_uint64(0)
     K = ctypes.c_uint64(0)
-    rc = _load().fcirc_plan_table(int(p), int(f) % int(p), int(n), s.ctypes.data, si.ctypes.data,
+    rc = _load().fcirc_plan_table(int(p), _scalar(f, p), int(n), s.ctypes.data, si.ctypes.data,
                                   ctypes.byref(w), ctypes.byref(K))
     _check(rc, "fcirc_plan_table")
     return s, si, int(w.value), int(K.value)

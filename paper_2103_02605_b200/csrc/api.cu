@@ -221,16 +221,18 @@ static int ilog2_exact(int64_t n) {
 // product path does not check this on the device.  In checking mode a counting kernel runs first
 // and the call synchronises the stream and returns FCIRC_EINVAL if any element is >= p.
 // ------------------------------------------------------------------------------------------
-template <class E>
+template <class E, bool PACKED>
 __global__ void k_count_noncanonical(const E* __restrict__ x, int64_t count, uint64_t p,
                                      unsigned long long* __restrict__ bad) {
   unsigned long long local = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-    local += (uint64_t)x[i] >= p;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = (uint64_t)x[i];
+    local += PACKED ? ((v & 0xFFFFFFFFull) >= p || (v >> 32) >= p) : v >= p;
+  }
   if (local) atomicAdd(bad, local);
 }
 
-static int check_canonical(uint64_t p, bool wide, const void* x, int64_t count, cudaStream_t st) {
+static int check_canonical(uint64_t p, const PrimeInfo* pi, const void* x, int64_t count, cudaStream_t st) {
   static const bool on = knob("CHECK_INPUTS", 0) != 0;
   if (!on || count <= 0) return FCIRC_OK;
   unsigned long long* d = nullptr;
@@ -238,8 +240,9 @@ static int check_canonical(uint64_t p, bool wide, const void* x, int64_t count, 
   if (cudaMallocAsync((void**)&d, sizeof h, st) != cudaSuccess) return FCIRC_ENOMEM;
   cudaMemsetAsync(d, 0, sizeof h, st);
   const unsigned blocks = (unsigned)std::min<int64_t>((count + 255) / 256, 148 * 8);
-  if (wide) k_count_noncanonical<uint64_t><<<blocks, 256, 0, st>>>((const uint64_t*)x, count, p, d);
-  else k_count_noncanonical<uint32_t><<<blocks, 256, 0, st>>>((const uint32_t*)x, count, p, d);
+  if (pi->kind == KIND_M31X2) k_count_noncanonical<uint64_t, true><<<blocks, 256, 0, st>>>((const uint64_t*)x, count, p, d);
+  else if (pi->wide) k_count_noncanonical<uint64_t, false><<<blocks, 256, 0, st>>>((const uint64_t*)x, count, p, d);
+  else k_count_noncanonical<uint32_t, false><<<blocks, 256, 0, st>>>((const uint32_t*)x, count, p, d);
   cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(d, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return FCIRC_ECUDA;
@@ -251,17 +254,23 @@ static int matvec_core(uint64_t p, uint64_t f, const void* a, const void* b, voi
                        cudaStream_t st, const EmbedIO& io) {
   const PrimeInfo* pi = prime_info(p);
   if (!pi) return FCIRC_EPRIME;
-  if (L > pi->two_adicity || L > max_log_n(pi->wide)) return FCIRC_ESIZE;
+  if (L > pi->two_adicity || L > max_log_n(pi->kind)) return FCIRC_ESIZE;
+  if (pi->kind != KIND_M31X2) f %= p;   // packed Z/p[sqrt 3] scalars are validated, not reduced
   // Theorem 1 premises checked on the host before touching the device
-  if (f % p == 0 || powmod(f % p, (p - 1) >> L, p) != 1) return FCIRC_ENOROOT;
+  int rc = check_premises(pi, f, L);
+  if (rc) return rc;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
   std::shared_ptr<DevPlan> dp;
-  int rc = get_plan(dev, p, f % p, L, &dp);
+  rc = get_plan(dev, p, f, L, &dp);
   if (rc) return rc;
-  if (pi->wide) {
+  if (pi->kind == KIND_GOLD) {
     FieldGold fld;
     return run_matvec_gold(fld, *dp, a, b, c, L, batch, st, dev, io);
+  }
+  if (pi->kind == KIND_M31X2) {
+    FieldM31x2 fld;
+    return run_matvec_m31(fld, *dp, a, b, c, L, batch, st, dev, io);
   }
   return run_matvec_u32(make_u32(p), *dp, a, b, c, L, batch, st, dev, io);
 }
@@ -275,11 +284,11 @@ static int matvec_impl(uint64_t p, uint64_t f, const void* a, const void* b, voi
   const PrimeInfo* pi = prime_info(p);
   if (!pi) return FCIRC_EPRIME;
   const size_t es = pi->wide ? 8 : 4;
-  if (L > pi->two_adicity || L > max_log_n(pi->wide)) return FCIRC_ESIZE;
+  if (L > pi->two_adicity || L > max_log_n(pi->kind)) return FCIRC_ESIZE;
   const size_t bytes = (size_t)n * (size_t)batch * es;
   if (overlaps(c, bytes, a, bytes) || overlaps(c, bytes, b, bytes)) return FCIRC_EINVAL;
-  int rc = check_canonical(p, pi->wide, a, n * batch, st);
-  if (rc == FCIRC_OK) rc = check_canonical(p, pi->wide, b, n * batch, st);
+  int rc = check_canonical(p, pi, a, n * batch, st);
+  if (rc == FCIRC_OK) rc = check_canonical(p, pi, b, n * batch, st);
   if (rc) return rc;
   return matvec_core(p, f, a, b, c, L, batch, st, EmbedIO{});
 }
@@ -450,14 +459,14 @@ int fcirc_circulant_matvec(uint64_t p, const void* a, const void* b, void* c, in
   const size_t bytes = (size_t)n * (size_t)batch * es;
   if (overlaps(c, bytes, a, bytes) || overlaps(c, bytes, b, bytes)) return FCIRC_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = check_canonical(p, pi->wide, a, n * batch, st);
-  if (rc == FCIRC_OK) rc = check_canonical(p, pi->wide, b, n * batch, st);
+  int rc = check_canonical(p, pi, a, n * batch, st);
+  if (rc == FCIRC_OK) rc = check_canonical(p, pi, b, n * batch, st);
   if (rc) return rc;
   if ((n & (n - 1)) == 0) return matvec_core(p, 1, a, b, c, ilog2_exact(n), batch, st, EmbedIO{});
   // Corollary 1: order N = the smallest power of two >= 2n - 1 (reading R10)
   const int64_t N = next_pow2(2 * n - 1);
   const int LN = ilog2_exact(N);
-  if (LN > pi->two_adicity || LN > max_log_n(pi->wide)) return FCIRC_ESIZE;
+  if (LN > pi->two_adicity || LN > max_log_n(pi->kind)) return FCIRC_ESIZE;
   EmbedIO io;
   io.mode = EMB_ANYN;
   io.na = n;
@@ -494,9 +503,9 @@ int fcirc_polymul(uint64_t p, const void* a, int64_t na, const void* b, int64_t 
       overlaps(c, (size_t)(nc * batch) * es, b, (size_t)(nb * batch) * es))
     return FCIRC_EINVAL;
   const int64_t L = next_pow2(nc);
-  if (ilog2_exact(L) > pi->two_adicity || ilog2_exact(L) > max_log_n(pi->wide)) return FCIRC_ESIZE;
-  int rc = check_canonical(p, pi->wide, a, na * batch, (cudaStream_t)stream);
-  if (rc == FCIRC_OK) rc = check_canonical(p, pi->wide, b, nb * batch, (cudaStream_t)stream);
+  if (ilog2_exact(L) > pi->two_adicity || ilog2_exact(L) > max_log_n(pi->kind)) return FCIRC_ESIZE;
+  int rc = check_canonical(p, pi, a, na * batch, (cudaStream_t)stream);
+  if (rc == FCIRC_OK) rc = check_canonical(p, pi, b, nb * batch, (cudaStream_t)stream);
   if (rc) return rc;
   return polymul_impl(p, a, na, b, nb, c, batch, (cudaStream_t)stream);
 }
@@ -539,8 +548,8 @@ int fcirc_schedule(uint64_t p, int64_t n, int* sub_log, int* top_levels) {
   if (L < 0) return FCIRC_EINVAL;
   const PrimeInfo* pi = prime_info(p);
   if (!pi) return FCIRC_EPRIME;
-  if (L > pi->two_adicity || L > max_log_n(pi->wide)) return FCIRC_ESIZE;
-  const int S = split_log_n(pi->wide, L);
+  if (L > pi->two_adicity || L > max_log_n(pi->kind)) return FCIRC_ESIZE;
+  const int S = split_log_n(pi->kind, L);
   *sub_log = L <= S ? L : S;
   *top_levels = L <= S ? 0 : L - S;
   return FCIRC_OK;

@@ -8,7 +8,11 @@ int run_matvec_gold(const FieldGold& fld, const DevPlan& dp, const void* a, cons
   return run_matvec(fld, dp, a, b, c, L, batch, st, dev, io);
 }
 
-int max_log_n(bool wide) { return (wide ? FTraits<FieldGold>::MMAX : FTraits<FieldU32>::MMAX) + KMAX; }
-int split_log_n(bool wide, int L) { return wide ? msplit<FieldGold>(L) : split_log_n_u32(L); }
+int max_log_n(int kind) {
+  return (kind == KIND_U32 ? FTraits<FieldU32>::MMAX : FTraits<FieldGold>::MMAX) + KMAX;   // M31: 13 as Gold
+}
+int split_log_n(int kind, int L) {
+  return kind == KIND_GOLD ? msplit<FieldGold>(L) : kind == KIND_M31X2 ? split_log_n_m31(L) : split_log_n_u32(L);
+}
 
 }  // namespace fcirc

@@ -37,6 +37,14 @@ template <> struct FTraits<FieldGold> {
   static constexpr const char* MS = "GOLD_MSPLIT";
   static constexpr int TMA_MIN_K = 9;
 };
+template <> struct FTraits<FieldM31x2> {      // the paper's ring, 8-byte packed elements (as Goldilocks)
+  static constexpr int MMAX = 13;
+  static constexpr int MPREF = 12;
+  static constexpr const char* RB = "M31_RB";
+  static constexpr const char* RC = "M31_RC";
+  static constexpr const char* MS = "M31_MSPLIT";
+  static constexpr int TMA_MIN_K = 9;
+};
 constexpr int KMAX = 11;
 
 // elements per thread (registers) for a transform of 2^M points; threads = 2^M / R
@@ -221,6 +229,7 @@ static int launch_cols_tma(const F& fld, ColArgs<F> args, int64_t instances, cud
 template <class F> struct RDefault;
 template <> struct RDefault<FieldU32> { static constexpr int RB = 8, RC = 16; };
 template <> struct RDefault<FieldGold> { static constexpr int RB = 8, RC = 8; };
+template <> struct RDefault<FieldM31x2> { static constexpr int RB = 8, RC = 8; };
 
 template <class F, int M>
 static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {

@@ -269,4 +269,64 @@ struct FieldGold {
   }
 };
 
+// ------------------------------------------------------------------------------------------
+// The paper's own ring: Z/pZ[sqrt 3], p = 2^31 - 1.  u + v sqrt 3 is packed as u | v << 32
+// with canonical components (< p).  (a + b sqrt 3)(c + d sqrt 3) = (ac + 3bd) + (ad + bc) sqrt 3;
+// the four 31x31-bit products and the sums fit in 64 bits (< 2^64), each component is then folded
+// with 2^31 == 1 (mod p) twice and canonicalised once.  Context only: it
+// reproduces the paper's arithmetic setting, the BASELINE configurations use Z/p.
+// ------------------------------------------------------------------------------------------
+struct FieldM31x2 {
+  using T = uint64_t;
+  using Tw = uint64_t;
+  static constexpr uint32_t P = 0x7FFFFFFFu;
+
+  __device__ __forceinline__ static uint32_t lo(uint64_t x) { return (uint32_t)x; }
+  __device__ __forceinline__ static uint32_t hi(uint64_t x) { return (uint32_t)(x >> 32); }
+  __device__ __forceinline__ static uint64_t pk(uint32_t u, uint32_t v) { return ((uint64_t)v << 32) | u; }
+  // x < 2^64 -> x mod p in [0, p)
+  __device__ __forceinline__ static uint32_t red(uint64_t x) {
+    x = (x & P) + (x >> 31);                 // < 2^31 + 2^33
+    x = (x & P) + (x >> 31);                 // <= 2^31 + 3
+    const uint32_t r = (uint32_t)x;
+    return r >= P ? r - P : r;
+  }
+  __device__ __forceinline__ static uint32_t addp(uint32_t a, uint32_t b) {
+    const uint32_t s = a + b;
+    return s >= P ? s - P : s;
+  }
+  __device__ __forceinline__ static uint32_t subp(uint32_t a, uint32_t b) { return a >= b ? a - b : a + P - b; }
+  __device__ __forceinline__ static uint64_t add(uint64_t x, uint64_t y) { return pk(addp(lo(x), lo(y)), addp(hi(x), hi(y))); }
+  __device__ __forceinline__ static uint64_t sub(uint64_t x, uint64_t y) { return pk(subp(lo(x), lo(y)), subp(hi(x), hi(y))); }
+  __device__ __forceinline__ static uint64_t mul(uint64_t x, uint64_t y) {
+    const uint64_t a = lo(x), b = hi(x), c = lo(y), d = hi(y);
+    return pk(red(a * c + 3 * (b * d)), red(a * d + b * c));
+  }
+
+  __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(y, s);
+    const uint64_t X = x;
+    x = add(X, t);
+    y = sub(X, t);
+  }
+  __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(x, s);
+    const uint64_t Y = y;
+    x = add(t, Y);
+    y = sub(t, Y);
+  }
+  __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
+    const uint64_t s = add(u, v), d = sub(u, v);
+    u = mul(s, si);
+    v = d;
+  }
+  __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
+    const uint64_t s = add(u, v), d = sub(u, v);
+    u = mul(s, si_k);
+    v = mul(d, k);
+  }
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const { return mul(mul(a, b), k); }
+};
+
 }  // namespace fcirc

@@ -17,12 +17,32 @@
 
 namespace fcirc {
 
+// Field kinds of the registry: the ring R of Theorem 1
+enum FieldKind { KIND_U32 = 0, KIND_GOLD = 1, KIND_M31X2 = 2 };
+
 struct PrimeInfo {
   uint64_t p;
-  int two_adicity;  // largest S with 2^S | p-1
-  uint64_t g;       // a generator of (Z/p)^*
-  bool wide;        // element type uint64 (Goldilocks) vs uint32
+  int two_adicity;  // largest S with 2^S | (group order): p-1, or p^2-1 for the quadratic extension
+  uint64_t g;       // a generator of (Z/p)^* (unused for KIND_M31X2)
+  bool wide;        // element type uint64 (Goldilocks, packed Z/p[sqrt 3]) vs uint32
+  int kind;         // FieldKind
 };
+
+// The paper's own ring: Z/pZ[sqrt 3], p = 2^31 - 1 (3 is a non-residue mod p).  An element
+// u + v sqrt 3 (u, v < p) is packed into a uint64 as u | v << 32.
+constexpr uint64_t kM31 = 0x7FFFFFFFull;
+struct Fp2 {
+  uint64_t u = 0, v = 0;
+};
+Fp2 fp2_unpack(uint64_t x);
+uint64_t fp2_pack(Fp2 a);
+Fp2 fp2_mul(Fp2 a, Fp2 b);
+Fp2 fp2_pow(Fp2 a, uint64_t e);
+Fp2 fp2_inv(Fp2 a);
+bool fp2_is_zero(Fp2 a);
+bool fp2_eq(Fp2 a, Fp2 b);
+// x is canonical (both components < p)
+bool fp2_canonical(uint64_t x);
 
 // nullptr if p is not in the registry
 const PrimeInfo* prime_info(uint64_t p);
@@ -45,7 +65,9 @@ struct HostPlan {
   uint64_t last_si = 0;        // s_{0,0}^-1 * K
 };
 
-// status: 0 ok, or FCIRC_ENOROOT / FCIRC_ESIZE
+// status: 0 ok, or FCIRC_ENOROOT / FCIRC_ESIZE (FCIRC_EINVAL: non-canonical packed f of Z/p[sqrt 3])
 int build_host_plan(uint64_t p, uint64_t f, int L, HostPlan* out);
+// Theorem 1 premises for a product of order 2^L with scalar f: FCIRC_OK / ESIZE / ENOROOT / EINVAL
+int check_premises(const PrimeInfo* pi, uint64_t f, int L);
 
 }  // namespace fcirc

@@ -45,11 +45,14 @@ int run_matvec_u32(const FieldU32& fld, const DevPlan& dp, const void* a, const 
                    int64_t batch, cudaStream_t st, int dev, const EmbedIO& io);
 int run_matvec_gold(const FieldGold& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
                     int64_t batch, cudaStream_t st, int dev, const EmbedIO& io);
+int run_matvec_m31(const FieldM31x2& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
+                   int64_t batch, cudaStream_t st, int dev, const EmbedIO& io);
 
-// largest supported log2 n of the executors (multi-pass: sub-problem size + KMAX)
-int max_log_n(bool wide);
+// largest supported log2 n of the executors (multi-pass: sub-problem size + KMAX); kind = FieldKind
+int max_log_n(int kind);
 // log2 of the on-chip sub-problem size for n = 2^L (L <= split: one fused pass; else sub-problems)
-int split_log_n(bool wide, int L);
+int split_log_n(int kind, int L);
 int split_log_n_u32(int L);
+int split_log_n_m31(int L);
 
 }  // namespace fcirc

@@ -27,14 +27,40 @@ P167 = 167772161            # 5 * 2^25 + 1
 GOLDILOCKS = (1 << 64) - (1 << 32) + 1
 PRIMES = (P998, P469, P167, GOLDILOCKS)
 BASE_SEED = 2103026050
+# the paper's own ring Z/pZ[sqrt 3], p = 2^31 - 1: elements u + v sqrt 3 packed u | v << 32
+M31X2 = (1 << 31) - 1
+
+
+def fp2_pack(u: int, v: int) -> int:
+    return (int(u) % M31X2) | ((int(v) % M31X2) << 32)
+
+
+def _fp2_mul(x: int, y: int) -> int:
+    """Only for the input definition f = w^n (as pow(w, n, p) for the prime fields)."""
+    u1, v1, u2, v2 = x & 0xFFFFFFFF, x >> 32, y & 0xFFFFFFFF, y >> 32
+    return fp2_pack(u1 * u2 + 3 * v1 * v2, u1 * v2 + u2 * v1)
+
+
+def fp2_pow(x: int, e: int) -> int:
+    r = 1
+    while e:
+        if e & 1:
+            r = _fp2_mul(r, x)
+        x = _fp2_mul(x, x)
+        e >>= 1
+    return r
 
 
 def dtype_for(p: int):
-    return np.uint32 if p < (1 << 32) else np.uint64
+    return np.uint64 if p >= (1 << 32) or p == M31X2 else np.uint32
 
 
 def uniform(rng: np.random.Generator, p: int, shape) -> np.ndarray:
-    """Uniform residues in [0, p) in the element dtype of p."""
+    """Uniform residues in [0, p) in the element dtype of p (both components for Z/p[sqrt 3])."""
+    if p == M31X2:
+        u = rng.integers(0, p, size=shape, dtype=np.uint64)
+        v = rng.integers(0, p, size=shape, dtype=np.uint64)
+        return u | (v << np.uint64(32))
     return rng.integers(0, p, size=shape, dtype=np.uint64).astype(dtype_for(p))
 
 
@@ -47,7 +73,19 @@ def matvec_inputs(p: int, n: int, batch: int, seed: int, f_mode: str = "wn"):
     """
     rng = np.random.default_rng(seed)
     w = int(rng.integers(1, p, dtype=np.uint64))
-    if f_mode == "wn":
+    if p == M31X2:   # w = w0 + w1 sqrt 3 (nonzero), f = w^n in Z/p[sqrt 3]
+        w = fp2_pack(w, int(rng.integers(0, p, dtype=np.uint64)))
+        if f_mode == "wn":
+            f = fp2_pow(w, n)
+        elif f_mode == "one":
+            w, f = 1, 1
+        elif f_mode == "minus_one":
+            w, f = None, fp2_pack(p - 1, 0)
+        elif f_mode == "random":
+            w, f = None, w
+        else:
+            raise ValueError(f_mode)
+    elif f_mode == "wn":
         f = pow(w, n, p)
     elif f_mode == "one":
         w, f = 1, 1
@@ -103,4 +141,8 @@ CONFIGS = {
                         seed=BASE_SEED + 3) for L in range(12, 23)},
     "C5": dict(kind="bigint", nwords=1 << 17, batch=8, seed=BASE_SEED + 4),
     "S1": dict(kind="matvec", p=P998, n=1 << 20, batch=64, f_mode="wn", seed=BASE_SEED + 5),
+    # S2 (context only): the paper's own experiment shape -- 10000 products of two
+    # n-coefficient polynomials in its ring Z/(2^31-1)[sqrt 3], n = 8 .. 512
+    **{f"S2_n{n}": dict(kind="polymul", p=M31X2, na=n, nb=n, batch=10000, seed=BASE_SEED + 6)
+       for n in (8, 16, 32, 64, 128, 256, 512)},
 }

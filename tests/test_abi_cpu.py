@@ -181,3 +181,67 @@ def test_circulant_any_n_validation_before_device():
     assert lib.fcirc_circulant_matvec(P998, 0, 2, 3, 5, 1, None) == -1        # null
     assert lib.fcirc_circulant_matvec(1000003, 1, 2, 3, 5, 1, None) == -2     # p not in the registry
     assert lib.fcirc_circulant_matvec(P998, 8, 8, 8, 5, 4, None) == -1        # c overlaps a
+
+
+# ---------------------------------------------------------------- the paper's ring Z/(2^31-1)[sqrt 3]
+
+M31 = fc.M31X2
+
+
+def _f2mul(x, y):
+    u1, v1, u2, v2 = x & 0xFFFFFFFF, x >> 32, y & 0xFFFFFFFF, y >> 32
+    return ((u1 * u2 + 3 * v1 * v2) % M31) | (((u1 * v2 + u2 * v1) % M31) << 32)
+
+
+def _f2pow(x, e):
+    r = 1
+    while e:
+        if e & 1:
+            r = _f2mul(r, x)
+        x = _f2mul(x, x)
+        e >>= 1
+    return r
+
+
+def _f2neg(x):
+    return ((M31 - (x & 0xFFFFFFFF)) % M31) | (((M31 - (x >> 32)) % M31) << 32)
+
+
+def test_m31x2_plan_table_structure():
+    """The twist table over the paper's ring: s_{d,e}^2 = f_{d,e}, children +-s,
+    s s^-1 = 1, w^n = f, K = n^-1, roots of unity from the paper's generator 2 + sqrt 3."""
+    rng = random.Random(31)
+    for L in [0, 1, 2, 5, 9]:
+        n = 1 << L
+        w0 = fc.fp2_pack(rng.randrange(1, M31), rng.randrange(M31))
+        for f in [1, fc.fp2_pack(M31 - 1, 0), _f2pow(w0, n)]:
+            s, si, w, K = fc.plan_table(M31, f, n)
+            assert _f2pow(w, n) == f
+            assert K == pow(n, -1, M31)
+            if L == 0:
+                continue
+            s = [int(x) for x in s]
+            si = [int(x) for x in si]
+            assert _f2mul(s[1], s[1]) == f
+            for d in range(1, L):
+                for e in range(1 << d):
+                    parent = s[(1 << (d - 1)) + (e >> 1)]
+                    fde = parent if e % 2 == 0 else _f2neg(parent)
+                    assert _f2mul(s[(1 << d) + e], s[(1 << d) + e]) == fde, (L, d, e)
+            for i in range(1, n):
+                assert _f2mul(s[i], si[i]) == 1
+
+
+def test_m31x2_premises():
+    lib = fc._load()
+    with pytest.raises(fc.FcircError) as ei:          # f = 0 has no inverse (P:52)
+        fc.plan_table(M31, 0, 16)
+    assert ei.value.code == -3
+    with pytest.raises(fc.FcircError) as ei:          # non-canonical packed scalar
+        fc.plan_table(M31, M31, 16)
+    assert ei.value.code == -1
+    with pytest.raises(fc.FcircError) as ei:          # a non-square is not a 16th power:
+        fc.plan_table(M31, fc.fp2_pack(1, 1), 16)     # norm(1 + sqrt 3) = -2, a non-residue (p = 7 mod 8)
+    assert ei.value.code == -3
+    assert fc.schedule(M31, 1 << 20) == (12, 8)
+    assert lib.fcirc_matvec(M31, 1, 1, 2, 3, 1 << 25, 1, None) == -4   # above the maximum

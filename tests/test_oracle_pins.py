@@ -379,3 +379,56 @@ def test_corollary1_embedding_any_n():
             assert len(a2) == N and len(b2) == N
             got = [int(v) for v in oracle.fcirc_entries(p, 1, a2, b2)][:n]
             assert got == ref, (n, N)
+
+
+# ---------------------------------------------------------------- the paper's ring
+
+def test_m31x2_paper_generator_and_ring():
+    """in Z/pZ[sqrt 3] (p = 2^31 - 1, 3 a non-residue) 2 + sqrt 3 generates the roots of unity:
+    its order is p + 1 = 2^31; sqrt 3 squares to 3."""
+    import oracle
+    M = oracle.M31
+    assert pow(3, (M - 1) // 2, M) == M - 1                      # 3 is a non-residue mod p
+    g = 2 | (1 << 32)
+    assert oracle.py_fp2_pow(g, 1 << 31) == 1
+    assert oracle.py_fp2_pow(g, 1 << 30) == M - 1                # -1: order exactly 2^31
+    assert oracle.py_fp2_mul(1 << 32, 1 << 32) == 3
+
+
+def test_m31x2_oracle_vs_python_witness_and_3x3():
+    """C oracle over Z/(2^31-1)[sqrt 3] = the Python-int witness; the 3x3 example's columns."""
+    import oracle
+    M = oracle.M31
+    rng = random.Random(77)
+    pk = lambda u, v: (u % M) | ((v % M) << 32)  # noqa: E731
+    for n in [1, 2, 3, 5, 8, 12]:
+        a = [pk(rng.randrange(M), rng.randrange(M)) for _ in range(n)]
+        b = [pk(rng.randrange(M), rng.randrange(M)) for _ in range(n)]
+        f = pk(rng.randrange(1, M), rng.randrange(M))
+        assert [int(x) for x in oracle.fcirc_entries_m31x2(f, a, b)] == oracle.py_fcirc_matvec_m31x2(f, a, b)
+    a = [pk(11, 1), pk(22, 2), pk(33, 3)]
+    f = pk(7, 5)
+    af = [oracle.py_fp2_mul(f, x) for x in a]
+    cols = [[a[0], af[2], af[1]], [a[1], a[0], af[2]], [a[2], a[1], a[0]]]   # column j of P:42-44
+    for j in range(3):
+        e = [0, 0, 0]
+        e[j] = 1
+        assert [int(x) for x in oracle.fcirc_entries_m31x2(f, a, e)] == cols[j]
+
+
+def test_m31x2_polymul_oracle_vs_python():
+    import oracle
+    M = oracle.M31
+    rng = random.Random(78)
+    pk = lambda u, v: (u % M) | ((v % M) << 32)  # noqa: E731
+    a = [pk(rng.randrange(M), rng.randrange(M)) for _ in range(9)]
+    b = [pk(rng.randrange(M), rng.randrange(M)) for _ in range(6)]
+    exp = []
+    for k in range(14):
+        au = av = 0
+        for i in range(max(0, k - 5), min(k, 8) + 1):
+            t = oracle.py_fp2_mul(a[i], b[k - i])
+            au += t & 0xFFFFFFFF
+            av += t >> 32
+        exp.append((au % M) | ((av % M) << 32))
+    assert [int(x) for x in oracle.polymul_coeffs_m31x2(a, b)] == exp

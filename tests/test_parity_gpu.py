@@ -377,3 +377,51 @@ def test_circulant_any_n_corollary1(p):
         for k in range(batch):
             exp = oracle.fcirc_entries(p, 1, inp["a"][k], inp["b"][k])
             assert np.array_equal(c[k].astype(np.uint64), exp), (n, k)
+
+
+# ---------------------------------------------------------------------------------- the paper's ring
+
+M31X2 = fc.M31X2
+
+
+@pytest.mark.parametrize("f_mode", ["wn", "one", "minus_one"])
+def test_m31x2_matvec_all_entries(f_mode):
+    """The f-circulant product over the paper's own ring Z/(2^31-1)[sqrt 3], every entry
+    against Definition 2 in that ring: fused sizes and the first multi-pass sizes."""
+    for L in list(range(0, 14)) + [15]:
+        batch = 3 if L <= 10 else 1
+        inp = synth.matvec_inputs(M31X2, 1 << L, batch, seed=600 + L, f_mode=f_mode)
+        c = run_matvec(inp)
+        for k in range(batch):
+            exp = oracle.fcirc_entries_m31x2(inp["f"], inp["a"][k], inp["b"][k])
+            got = c[k].astype(np.uint64)
+            bad = np.nonzero(got != exp)[0]
+            assert bad.size == 0, (L, k, bad[:4])
+
+
+def test_m31x2_matvec_multipass_sampled():
+    for L in range(16, 21):
+        inp = synth.matvec_inputs(M31X2, 1 << L, 2, seed=650 + L)
+        c = run_matvec(inp)
+        for k in range(2):
+            idx = synth.sample_indices(1 << L, 512, seed=k)
+            exp = oracle.fcirc_entries_m31x2(inp["f"], inp["a"][k], inp["b"][k], idx)
+            assert np.array_equal(c[k][idx].astype(np.uint64), exp), (L, k)
+
+
+def test_m31x2_polymul_paper_shapes():
+    """The paper's experiment: products of two n-coefficient polynomials, n = 8..512,
+    in Z/(2^31-1)[sqrt 3] -- every coefficient against the schoolbook oracle."""
+    for n in [8, 16, 32, 64, 128, 256, 512, 3000]:
+        pin = synth.polymul_inputs(M31X2, n, n, 4, seed=n)
+        c = _host(fc.polymul(_dev(pin["a"]), _dev(pin["b"]), M31X2))
+        for k in range(4):
+            assert np.array_equal(c[k].astype(np.uint64), oracle.polymul_coeffs_m31x2(pin["a"][k], pin["b"][k])), (n, k)
+
+
+def test_m31x2_circulant_any_n():
+    for n in [3, 7, 100, 1000]:
+        inp = synth.matvec_inputs(M31X2, n, 2, seed=700 + n, f_mode="one")
+        c = _host(fc.circulant_matvec(_dev(inp["a"]), _dev(inp["b"]), M31X2))
+        for k in range(2):
+            assert np.array_equal(c[k].astype(np.uint64), oracle.fcirc_entries_m31x2(1, inp["a"][k], inp["b"][k]))
