@@ -250,11 +250,14 @@ struct FieldGold {
     x = add_c(Y, t);
     y = sub_w(t, Y);
   }
-  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical
+  // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical.
+  // Select forms: in the isolated-butterfly microbenchmark the mask forms were faster for this
+  // butterfly, but inside k_block (mixed with the forward butterflies, FMA-heavy pipe at 80 %)
+  // the select forms measured 1.6 % faster (profiles/r01f_sweep_gold_inv_select.txt).
   __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
-    const uint64_t s = add_c_m(u, v);   // u + v < 2p: one correction, result weak
-    const uint64_t d = sub_c(u, v);     // canonical
-    u = mul_m(s, si);
+    const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
+    const uint64_t d = sub_c(u, v);   // canonical
+    u = mul(s, si);
     v = d;
   }
   __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
