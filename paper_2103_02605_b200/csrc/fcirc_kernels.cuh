@@ -124,6 +124,76 @@ __device__ __forceinline__ void io_store(T* dst, int64_t inst, int64_t pos, int6
 }
 
 // ------------------------------------------------------------------------------------------
+// Building blocks of the register/shared-memory phase scheme, shared by every kernel below.
+//   exchange / exchange2  move the R register values of one (or two) arrays from the layout of
+//                         phase ph_from to that of ph_to through shared memory; idx(base, slot)
+//                         maps an address (k_block: position, k_cols: row) given as its thread
+//                         part plus its compile-time slot part to the swizzled smem index
+//   forward_phase         the split levels of phase ph, top address bit first: bf(s0, s1, bit, x)
+//                         gets the two slots of a butterfly pair, the pair bit and the address
+//   inverse_phase         the recombination levels of phase ph, low address bit first
+// All loops are fully unrolled (compile-time slots), so the register arrays stay in registers.
+// ------------------------------------------------------------------------------------------
+template <class PH, int R, class T, class Idx>
+__device__ __forceinline__ void exchange(T (&x)[R], T* buf, int ph_from, int ph_to, int t, Idx idx) {
+  const int wb = PH::ins_t(ph_from, t);
+#pragma unroll
+  for (int s = 0; s < R; ++s) buf[idx(wb, PH::cslot(ph_from, s))] = x[s];
+  __syncthreads();
+  const int rb = PH::ins_t(ph_to, t);
+#pragma unroll
+  for (int s = 0; s < R; ++s) x[s] = buf[idx(rb, PH::cslot(ph_to, s))];
+  __syncthreads();
+}
+
+template <class PH, int R, class T, class Idx>
+__device__ __forceinline__ void exchange2(T (&x)[R], T (&y)[R], T* bx, T* by, int ph_from, int ph_to, int t, Idx idx) {
+  const int wb = PH::ins_t(ph_from, t);
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int ad = idx(wb, PH::cslot(ph_from, s));
+    bx[ad] = x[s];
+    by[ad] = y[s];
+  }
+  __syncthreads();
+  const int rb = PH::ins_t(ph_to, t);
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int ad = idx(rb, PH::cslot(ph_to, s));
+    x[s] = bx[ad];
+    y[s] = by[ad];
+  }
+  __syncthreads();
+}
+
+template <class PH, int R, class BF>
+__device__ __forceinline__ void forward_phase(int ph, int t, BF bf) {
+  const int rp = PH::rp(ph), lo = PH::lo(ph), tins = PH::ins_t(ph, t);
+#pragma unroll
+  for (int l = 0; l < rp; ++l) {
+    const int jb = rp - 1 - l;
+#pragma unroll
+    for (int s0 = 0; s0 < R; ++s0) {
+      if ((s0 >> jb) & 1) continue;
+      bf(s0, s0 + (1 << jb), lo + jb, tins | PH::cslot(ph, s0));
+    }
+  }
+}
+
+template <class PH, int R, class BF>
+__device__ __forceinline__ void inverse_phase(int ph, int t, BF bf) {
+  const int rp = PH::rp(ph), lo = PH::lo(ph), tins = PH::ins_t(ph, t);
+#pragma unroll
+  for (int jb = 0; jb < rp; ++jb) {
+#pragma unroll
+    for (int s0 = 0; s0 < R; ++s0) {
+      if ((s0 >> jb) & 1) continue;
+      bf(s0, s0 + (1 << jb), lo + jb, tins | PH::cslot(ph, s0));
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // k_block: fused sub-problem kernel
 // ------------------------------------------------------------------------------------------
 template <class F>
@@ -157,14 +227,15 @@ k_block(F fld, BlockArgs<F> args) {
   constexpr int m = 1 << M;
   constexpr int TT = PH::T;
   constexpr int NPH = PH::NPH;
-  constexpr int PM = m;  // length of one array in smem (swizzled, unpadded)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* sm = reinterpret_cast<T*>(smem_raw);
 
   const int t = threadIdx.x % TT;
   const int li = threadIdx.x / TT;
-  T* sa = sm + (size_t)li * 2 * PM;
-  T* sb = sa + PM;
+  T* sa = sm + (size_t)li * 2 * m;   // swizzled, unpadded
+  T* sb = sa + m;
+  // swz is GF(2)-linear: swz(base | slot) = swz(base) ^ swz(slot), the latter a compile-time constant
+  auto idx = [](int base_part, int slot_part) { return swz<R, T>(base_part) ^ swz<R, T>(slot_part); };
 
   const int k = args.k;
   const int E = (int)(blockIdx.x & ((1u << k) - 1));   // sub-block index
@@ -180,7 +251,7 @@ k_block(F fld, BlockArgs<F> args) {
   // butterflies read twiddles with LDS instead of scattered L2 loads (profiles/r01c: the u32
   // k_block stalled on long_scoreboard).  Goldilocks is arithmetic-bound and keeps the LDG path;
   // so does the fused whole-product launch (k = 0), whose CTAs all share one table via L1/L2.
-  Tw* twsf = reinterpret_cast<Tw*>(sm + (size_t)IPC * 2 * PM);
+  Tw* twsf = reinterpret_cast<Tw*>(sm + (size_t)IPC * 2 * m);
   Tw* twsi = twsf + m;
   if constexpr (TWS) {
     for (int q = threadIdx.x; q < m - 1; q += blockDim.x) {
@@ -192,72 +263,44 @@ k_block(F fld, BlockArgs<F> args) {
     }
     __syncthreads();
   }
-  auto twf_at = [&](int ph_bbit, int xaddr) -> Tw {   // forward twiddle of pair bit b at address x
-    if constexpr (TWS) return twsf[tw_swz((1 << (M - 1 - ph_bbit)) - 1 + (xaddr >> (ph_bbit + 1)))];
-    else return args.twf[(gbase | xaddr) >> (ph_bbit + 1)];
+  // twiddle of the pair bit `bit` at address x: heap entry (2^k + E) 2^(M-1-bit) + (x >> (bit+1))
+  auto twf_at = [&](int bit, int x) -> Tw {
+    if constexpr (TWS) return twsf[tw_swz((1 << (M - 1 - bit)) - 1 + (x >> (bit + 1)))];
+    else return args.twf[(gbase | x) >> (bit + 1)];
   };
-  auto twi_at = [&](int ph_bbit, int xaddr) -> Tw {
-    if constexpr (TWS) return twsi[tw_swz((1 << (M - 1 - ph_bbit)) - 1 + (xaddr >> (ph_bbit + 1)))];
-    else return args.twi[(gbase | xaddr) >> (ph_bbit + 1)];
+  auto twi_at = [&](int bit, int x) -> Tw {
+    if constexpr (TWS) return twsi[tw_swz((1 << (M - 1 - bit)) - 1 + (x >> (bit + 1)))];
+    else return args.twi[(gbase | x) >> (bit + 1)];
   };
 
   T xa[R], xb[R];
   // ---- load (phase-0 addresses: slot s at s * 2^lo + t, coalesced across t)
-  if (active && !EMB) {
+  if (active) {
 #pragma unroll
     for (int s = 0; s < R; ++s) {
       const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
-      xa[s] = args.a[base + ad];
-      xb[s] = args.b[base + ad];
-    }
-  } else if (active) {
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
-      xa[s] = io_load(args.a, inst, ad, m, false, args.io);
-      xb[s] = io_load(args.b, inst, ad, m, true, args.io);
+      if constexpr (EMB) {
+        xa[s] = io_load(args.a, inst, ad, m, false, args.io);
+        xb[s] = io_load(args.b, inst, ad, m, true, args.io);
+      } else {
+        xa[s] = args.a[base + ad];
+        xb[s] = args.b[base + ad];
+      }
     }
   } else {
 #pragma unroll
-    for (int s = 0; s < R; ++s) { xa[s] = 0; xb[s] = 0; }
+    for (int s = 0; s < R; ++s) xa[s] = xb[s] = 0;
   }
 
-  // ---- forward levels (Algorithm 1 split of a and b), phase by phase
+  // ---- forward levels (Algorithm 1 split of a and b, sharing each twiddle), phase by phase
 #pragma unroll
   for (int ph = 0; ph < NPH; ++ph) {
-    if (ph > 0) {
-      const int wb = PH::ins_t(ph - 1, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int ad = swz<R, T>(wb) ^ swz<R, T>(PH::cslot(ph - 1, s));
-        sa[ad] = xa[s];
-        sb[ad] = xb[s];
-      }
-      __syncthreads();
-      const int rb = PH::ins_t(ph, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int ad = swz<R, T>(rb) ^ swz<R, T>(PH::cslot(ph, s));
-        xa[s] = sa[ad];
-        xb[s] = sb[ad];
-      }
-      __syncthreads();
-    }
-    const int rp = PH::rp(ph), lo = PH::lo(ph);
-    const int tb = PH::ins_t(ph, t);
-#pragma unroll
-    for (int l = 0; l < rp; ++l) {
-      const int jb = rp - 1 - l;
-      const int bbit = lo + jb;
-#pragma unroll
-      for (int s0 = 0; s0 < R; ++s0) {
-        if ((s0 >> jb) & 1) continue;
-        const int s1 = s0 + (1 << jb);
-        const Tw tw = twf_at(bbit, tb | PH::cslot(ph, s0));
-        fld.fwd_a(xa[s0], xa[s1], tw);
-        fld.fwd_b(xb[s0], xb[s1], tw);
-      }
-    }
+    if (ph > 0) exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx);
+    forward_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int x) {
+      const Tw tw = twf_at(bit, x);
+      fld.fwd_a(xa[s0], xa[s1], tw);
+      fld.fwd_b(xb[s0], xb[s1], tw);
+    });
   }
 
   // ---- leaves: 1x1 products (the recursion bottom), same thread/slot layout
@@ -268,57 +311,35 @@ k_block(F fld, BlockArgs<F> args) {
       else args.out[base] = v;
     }
   } else {
-  T xm[R];
+    T xm[R];
 #pragma unroll
-  for (int s = 0; s < R; ++s) xm[s] = fld.leaf(xa[s], xb[s]);
+    for (int s = 0; s < R; ++s) xm[s] = fld.leaf(xa[s], xb[s]);
 
-  // ---- inverse levels (recombination c1 = (M1+M2)/(2s), c2 = (M1-M2)/2), low bits first
-  const bool top = (k == 0);
+    // ---- inverse levels (recombination c1 = (M1+M2)/(2s), c2 = (M1-M2)/2), low bits first
+    const bool top = (k == 0);
 #pragma unroll
-  for (int ph = NPH - 1; ph >= 0; --ph) {
-    if (ph < NPH - 1) {
-      const int wb = PH::ins_t(ph + 1, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) sa[swz<R, T>(wb) ^ swz<R, T>(PH::cslot(ph + 1, s))] = xm[s];
-      __syncthreads();
-      const int rb = PH::ins_t(ph, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) xm[s] = sa[swz<R, T>(rb) ^ swz<R, T>(PH::cslot(ph, s))];
-      __syncthreads();
+    for (int ph = NPH - 1; ph >= 0; --ph) {
+      if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx);
+      inverse_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int x) {
+        if (bit == M - 1 && top) fld.inv_last(xm[s0], xm[s1], args.last_si, args.last_k);
+        else fld.inv(xm[s0], xm[s1], twi_at(bit, x));
+      });
     }
-    const int rp = PH::rp(ph), lo = PH::lo(ph);
-    const int tb = PH::ins_t(ph, t);
+
+    // ---- store (phase-0 addresses, coalesced)
+    if (active) {
 #pragma unroll
-    for (int l = 0; l < rp; ++l) {
-      const int jb = l;
-      const int bbit = lo + jb;
-#pragma unroll
-      for (int s0 = 0; s0 < R; ++s0) {
-        if ((s0 >> jb) & 1) continue;
-        const int s1 = s0 + (1 << jb);
-        if (bbit == M - 1 && top) {
-          fld.inv_last(xm[s0], xm[s1], args.last_si, args.last_k);
-        } else {
-          const Tw tw = twi_at(bbit, tb | PH::cslot(ph, s0));
-          fld.inv(xm[s0], xm[s1], tw);
-        }
+      for (int s = 0; s < R; ++s) {
+        const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
+        if constexpr (EMB) io_store(args.out, inst, ad, m, xm[s], args.io);
+        else args.out[base + ad] = xm[s];
       }
     }
   }
-
-  // ---- store (phase-0 addresses, coalesced)
-  if (active && (!EMB || !emb_truncates(args.io.mode))) {
-#pragma unroll
-    for (int s = 0; s < R; ++s) args.out[base + PH::ins_t(0, t) + PH::cslot(0, s)] = xm[s];
-  } else if (active) {
-#pragma unroll
-    for (int s = 0; s < R; ++s) io_store(args.out, inst, PH::ins_t(0, t) + PH::cslot(0, s), m, xm[s], args.io);
-  }
-  }  // M > 0
 }
 
 // ------------------------------------------------------------------------------------------
-// k_cols: the top K levels, along columns of stride m = n / 2^K
+// Column passes: the top K levels, along columns of stride m = n / 2^K
 // ------------------------------------------------------------------------------------------
 template <class F>
 struct ColArgs {
@@ -328,7 +349,7 @@ struct ColArgs {
   typename F::T* dst1;        // forward: b'
   int64_t m;                  // column stride = n >> K
   int64_t n;
-  int64_t colblocks;          // m / W
+  int64_t colblocks;          // m / (W * column groups per thread)
   int64_t units;              // instances * colblocks
   const typename F::Tw* twf;
   const typename F::Tw* twi;
@@ -337,6 +358,47 @@ struct ColArgs {
   EmbedIO io;                 // EMB only: forward embedding of the loads; inverse truncation of the stores
 };
 
+// row swizzle (GF(2)-linear bijection of [0, 2^K)): with the short phase on top, the rows a warp
+// touches in one access land in distinct banks in every phase (tools/bank_model.py)
+template <class PH, int W>
+struct ColIdx {
+  int c;
+  __device__ __forceinline__ int operator()(int row) const { return (row ^ ((row >> PH::r) & 7)) * W + c; }
+  __device__ __forceinline__ int operator()(int base_part, int slot_part) const { return (*this)(base_part + slot_part); }
+};
+
+// twiddles of the column levels: heap entry (2^K | row) >> (bit + 1), the same for every column
+template <int K, class Tw>
+__device__ __forceinline__ Tw col_tw(const Tw* table, int bit, int row) {
+  return table[((1 << K) | row) >> (bit + 1)];
+}
+
+// The K forward levels of NG register arrays (same rows), NG in {1, 2}: bf runs the butterflies.
+template <class PH, int K, int R, int NPH, class T, class Idx, class BF>
+__device__ __forceinline__ void col_forward(T (&x)[R], T (*y)[R], T* bx, T* by, int t, Idx idx, BF bf) {
+#pragma unroll
+  for (int ph = 0; ph < NPH; ++ph) {
+    if (ph > 0) {
+      if (y) exchange2<PH, R>(x, *y, bx, by, ph - 1, ph, t, idx);
+      else exchange<PH, R>(x, bx, ph - 1, ph, t, idx);
+    }
+    forward_phase<PH, R>(ph, t, bf);
+  }
+}
+
+template <class PH, int K, int R, int NPH, class T, class Idx, class BF>
+__device__ __forceinline__ void col_inverse(T (&x)[R], T (*y)[R], T* bx, T* by, int t, Idx idx, BF bf) {
+#pragma unroll
+  for (int ph = NPH - 1; ph >= 0; --ph) {
+    if (ph < NPH - 1) {
+      if (y) exchange2<PH, R>(x, *y, bx, by, ph + 1, ph, t, idx);
+      else exchange<PH, R>(x, bx, ph + 1, ph, t, idx);
+    }
+    inverse_phase<PH, R>(ph, t, bf);
+  }
+}
+
+// k_cols: one operand per thread; the forward pass covers a (blockIdx.y = 0) and b (= 1)
 template <class F, int K, int R, int W, bool INV, int MINB = 1, bool EMB = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols(F fld, ColArgs<F> args) {
@@ -349,112 +411,42 @@ k_cols(F fld, ColArgs<F> args) {
 
   const int c = threadIdx.x % W;
   const int t = threadIdx.x / W;
-  const int64_t unit = blockIdx.x;
-  const int64_t inst = unit / args.colblocks;
-  const int64_t cb = unit - inst * args.colblocks;
-  const int64_t col = cb * W + c;
+  const int64_t inst = blockIdx.x / args.colblocks;
+  const int64_t col = (blockIdx.x - inst * args.colblocks) * W + c;
   const int64_t base = inst * args.n + col;
   const int64_t m = args.m;
-  const bool second = (!INV) && blockIdx.y == 1;   // forward: y = 0 -> a, y = 1 -> b
+  const bool second = (!INV) && blockIdx.y == 1;
   const T* src = second ? args.src1 : args.src0;
   T* dst = second ? args.dst1 : args.dst0;
-
-  // row swizzle (GF(2)-linear bijection of [0, 2^K)): with the short phase on top, the rows a warp
-  // touches in one access land in distinct banks in every phase (tools/bank_model.py)
-  auto sidx = [&](int row) { return (row ^ ((row >> PH::r) & 7)) * W + c; };
+  const ColIdx<PH, W> idx{c};
 
   T x[R];
-  const int ph_first = INV ? NPH - 1 : 0;
-  {
-    const int rb = PH::ins_t(ph_first, t);
+  const int ph_in = INV ? NPH - 1 : 0, ph_out = INV ? 0 : NPH - 1;
 #pragma unroll
-    if (INV || !EMB) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) x[s] = src[base + (int64_t)(rb + PH::cslot(ph_first, s)) * m];
-    } else {
-#pragma unroll
-      for (int s = 0; s < R; ++s)
-        x[s] = io_load(src, inst, col + (int64_t)(rb + PH::cslot(ph_first, s)) * m, args.n, second, args.io);
-    }
+  for (int s = 0; s < R; ++s) {
+    const int64_t row = PH::ins_t(ph_in, t) + PH::cslot(ph_in, s);
+    if constexpr (EMB && !INV) x[s] = io_load(src, inst, col + row * m, args.n, second, args.io);
+    else x[s] = src[base + row * m];
   }
-
-  if (!INV) {
-#pragma unroll
-    for (int ph = 0; ph < NPH; ++ph) {
-      if (ph > 0) {
-        const int wb = PH::ins_t(ph - 1, t);
-#pragma unroll
-        for (int s = 0; s < R; ++s) sm[sidx(wb + PH::cslot(ph - 1, s))] = x[s];
-        __syncthreads();
-        const int rb = PH::ins_t(ph, t);
-#pragma unroll
-        for (int s = 0; s < R; ++s) x[s] = sm[sidx(rb + PH::cslot(ph, s))];
-        __syncthreads();
-      }
-      const int rp = PH::rp(ph), lo = PH::lo(ph);
-      const int tb = (1 << K) | PH::ins_t(ph, t);
-#pragma unroll
-      for (int l = 0; l < rp; ++l) {
-        const int jb = rp - 1 - l;
-        const int bbit = lo + jb;
-        const int tsh = tb >> (bbit + 1);
-#pragma unroll
-        for (int s0 = 0; s0 < R; ++s0) {
-          if ((s0 >> jb) & 1) continue;
-          const int s1 = s0 + (1 << jb);
-          const Tw tw = args.twf[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
-          if (second) fld.fwd_b(x[s0], x[s1], tw);
-          else fld.fwd_a(x[s0], x[s1], tw);
-        }
-      }
-    }
-    const int rb = PH::ins_t(NPH - 1, t);
-#pragma unroll
-    for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(NPH - 1, s)) * m] = x[s];
+  if constexpr (!INV) {
+    col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int row) {
+      const Tw tw = col_tw<K>(args.twf, bit, row);
+      if (second) fld.fwd_b(x[s0], x[s1], tw);
+      else fld.fwd_a(x[s0], x[s1], tw);
+    });
   } else {
+    col_inverse<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int row) {
+      if (bit == K - 1) fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
+      else fld.inv(x[s0], x[s1], col_tw<K>(args.twi, bit, row));
+    });
+  }
 #pragma unroll
-    for (int ph = NPH - 1; ph >= 0; --ph) {
-      if (ph < NPH - 1) {
-        const int wb = PH::ins_t(ph + 1, t);
-#pragma unroll
-        for (int s = 0; s < R; ++s) sm[sidx(wb + PH::cslot(ph + 1, s))] = x[s];
-        __syncthreads();
-        const int rb = PH::ins_t(ph, t);
-#pragma unroll
-        for (int s = 0; s < R; ++s) x[s] = sm[sidx(rb + PH::cslot(ph, s))];
-        __syncthreads();
-      }
-      const int rp = PH::rp(ph), lo = PH::lo(ph);
-      const int tb = (1 << K) | PH::ins_t(ph, t);
-#pragma unroll
-      for (int l = 0; l < rp; ++l) {
-        const int jb = l;
-        const int bbit = lo + jb;
-        const int tsh = tb >> (bbit + 1);
-#pragma unroll
-        for (int s0 = 0; s0 < R; ++s0) {
-          if ((s0 >> jb) & 1) continue;
-          const int s1 = s0 + (1 << jb);
-          if (bbit == K - 1) {
-            fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
-          } else {
-            const Tw tw = args.twi[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
-            fld.inv(x[s0], x[s1], tw);
-          }
-        }
-      }
-    }
-    const int rb = PH::ins_t(0, t);
-    if (!EMB || !emb_truncates(args.io.mode)) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(0, s)) * m] = x[s];
-    } else {
-#pragma unroll
-      for (int s = 0; s < R; ++s) io_store(dst, inst, col + (int64_t)(rb + PH::cslot(0, s)) * m, args.n, x[s], args.io);
-    }
+  for (int s = 0; s < R; ++s) {
+    const int64_t row = PH::ins_t(ph_out, t) + PH::cslot(ph_out, s);
+    if constexpr (EMB && INV) io_store(dst, inst, col + row * m, args.n, x[s], args.io);
+    else dst[base + row * m] = x[s];
   }
 }
-
 
 // ------------------------------------------------------------------------------------------
 // k_cols_fwd2: the forward column pass for a AND b in the same thread (like k_block): each twiddle
@@ -475,74 +467,32 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
 
   const int c = threadIdx.x % W;
   const int t = threadIdx.x / W;
-  const int64_t unit = blockIdx.x;
-  const int64_t inst = unit / args.colblocks;
-  const int64_t cb = unit - inst * args.colblocks;
-  const int64_t col = cb * W + c;
+  const int64_t inst = blockIdx.x / args.colblocks;
+  const int64_t col = (blockIdx.x - inst * args.colblocks) * W + c;
   const int64_t base = inst * args.n + col;
   const int64_t m = args.m;
-  auto sidx = [&](int row) { return (row ^ ((row >> PH::r) & 7)) * W + c; };
+  const ColIdx<PH, W> idx{c};
 
   T xa[R], xb[R];
-  {
-    const int rb = PH::ins_t(0, t);
-    if (!EMB) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int64_t ad = base + (int64_t)(rb + PH::cslot(0, s)) * m;
-        xa[s] = args.src0[ad];
-        xb[s] = args.src1[ad];
-      }
-    } else {
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int64_t pos = col + (int64_t)(rb + PH::cslot(0, s)) * m;
-        xa[s] = io_load(args.src0, inst, pos, args.n, false, args.io);
-        xb[s] = io_load(args.src1, inst, pos, args.n, true, args.io);
-      }
-    }
-  }
-#pragma unroll
-  for (int ph = 0; ph < NPH; ++ph) {
-    if (ph > 0) {
-      const int wb = PH::ins_t(ph - 1, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int ad = sidx(wb + PH::cslot(ph - 1, s));
-        sma[ad] = xa[s];
-        smb[ad] = xb[s];
-      }
-      __syncthreads();
-      const int rb = PH::ins_t(ph, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int ad = sidx(rb + PH::cslot(ph, s));
-        xa[s] = sma[ad];
-        xb[s] = smb[ad];
-      }
-      __syncthreads();
-    }
-    const int rp = PH::rp(ph), lo = PH::lo(ph);
-    const int tb = (1 << K) | PH::ins_t(ph, t);
-#pragma unroll
-    for (int l = 0; l < rp; ++l) {
-      const int jb = rp - 1 - l;
-      const int bbit = lo + jb;
-      const int tsh = tb >> (bbit + 1);
-#pragma unroll
-      for (int s0 = 0; s0 < R; ++s0) {
-        if ((s0 >> jb) & 1) continue;
-        const int s1 = s0 + (1 << jb);
-        const Tw tw = args.twf[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
-        fld.fwd_a(xa[s0], xa[s1], tw);
-        fld.fwd_b(xb[s0], xb[s1], tw);
-      }
-    }
-  }
-  const int rb = PH::ins_t(NPH - 1, t);
 #pragma unroll
   for (int s = 0; s < R; ++s) {
-    const int64_t ad = base + (int64_t)(rb + PH::cslot(NPH - 1, s)) * m;
+    const int64_t row = PH::ins_t(0, t) + PH::cslot(0, s);
+    if constexpr (EMB) {
+      xa[s] = io_load(args.src0, inst, col + row * m, args.n, false, args.io);
+      xb[s] = io_load(args.src1, inst, col + row * m, args.n, true, args.io);
+    } else {
+      xa[s] = args.src0[base + row * m];
+      xb[s] = args.src1[base + row * m];
+    }
+  }
+  col_forward<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int row) {
+    const Tw tw = col_tw<K>(args.twf, bit, row);
+    fld.fwd_a(xa[s0], xa[s1], tw);
+    fld.fwd_b(xb[s0], xb[s1], tw);
+  });
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int64_t ad = base + (int64_t)(PH::ins_t(NPH - 1, t) + PH::cslot(NPH - 1, s)) * m;
     args.dst0[ad] = xa[s];
     args.dst1[ad] = xb[s];
   }
@@ -565,69 +515,31 @@ k_cols_inv2(F fld, ColArgs<F> args) {
 
   const int c = threadIdx.x % W;
   const int t = threadIdx.x / W;
-  const int64_t unit = blockIdx.x;
-  const int64_t inst = unit / args.colblocks;     // colblocks = m / (2 W)
-  const int64_t cb = unit - inst * args.colblocks;
-  const int64_t base = inst * args.n + cb * 2 * W + c;
+  const int64_t inst = blockIdx.x / args.colblocks;     // colblocks = m / (2 W)
+  const int64_t base = inst * args.n + (blockIdx.x - inst * args.colblocks) * 2 * W + c;
   const int64_t m = args.m;
-  auto sidx = [&](int row) { return (row ^ ((row >> PH::r) & 7)) * W + c; };
+  const ColIdx<PH, W> idx{c};
 
   T xa[R], xb[R];
-  {
-    const int rb = PH::ins_t(NPH - 1, t);
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      const int64_t ad = base + (int64_t)(rb + PH::cslot(NPH - 1, s)) * m;
-      xa[s] = args.src0[ad];
-      xb[s] = args.src0[ad + W];
-    }
-  }
-#pragma unroll
-  for (int ph = NPH - 1; ph >= 0; --ph) {
-    if (ph < NPH - 1) {
-      const int wb = PH::ins_t(ph + 1, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int ad = sidx(wb + PH::cslot(ph + 1, s));
-        sma[ad] = xa[s];
-        smb[ad] = xb[s];
-      }
-      __syncthreads();
-      const int rb = PH::ins_t(ph, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        const int ad = sidx(rb + PH::cslot(ph, s));
-        xa[s] = sma[ad];
-        xb[s] = smb[ad];
-      }
-      __syncthreads();
-    }
-    const int rp = PH::rp(ph), lo = PH::lo(ph);
-    const int tb = (1 << K) | PH::ins_t(ph, t);
-#pragma unroll
-    for (int l = 0; l < rp; ++l) {
-      const int jb = l;
-      const int bbit = lo + jb;
-      const int tsh = tb >> (bbit + 1);
-#pragma unroll
-      for (int s0 = 0; s0 < R; ++s0) {
-        if ((s0 >> jb) & 1) continue;
-        const int s1 = s0 + (1 << jb);
-        if (bbit == K - 1) {
-          fld.inv_last(xa[s0], xa[s1], args.last_si, args.last_k);
-          fld.inv_last(xb[s0], xb[s1], args.last_si, args.last_k);
-        } else {
-          const Tw tw = args.twi[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
-          fld.inv(xa[s0], xa[s1], tw);
-          fld.inv(xb[s0], xb[s1], tw);
-        }
-      }
-    }
-  }
-  const int rb = PH::ins_t(0, t);
 #pragma unroll
   for (int s = 0; s < R; ++s) {
-    const int64_t ad = base + (int64_t)(rb + PH::cslot(0, s)) * m;
+    const int64_t ad = base + (int64_t)(PH::ins_t(NPH - 1, t) + PH::cslot(NPH - 1, s)) * m;
+    xa[s] = args.src0[ad];
+    xb[s] = args.src0[ad + W];
+  }
+  col_inverse<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int row) {
+    if (bit == K - 1) {
+      fld.inv_last(xa[s0], xa[s1], args.last_si, args.last_k);
+      fld.inv_last(xb[s0], xb[s1], args.last_si, args.last_k);
+    } else {
+      const Tw tw = col_tw<K>(args.twi, bit, row);
+      fld.inv(xa[s0], xa[s1], tw);
+      fld.inv(xb[s0], xb[s1], tw);
+    }
+  });
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    const int64_t ad = base + (int64_t)(PH::ins_t(0, t) + PH::cslot(0, s)) * m;
     args.dst0[ad] = xa[s];
     args.dst0[ad + W] = xb[s];
   }
@@ -692,7 +604,7 @@ k_cols_tma(F fld, ColArgs<F> args, const __grid_constant__ CUtensorMap map0, con
   const int c = threadIdx.x % W;
   const int t = threadIdx.x / W;
   const int64_t m = args.m;
-  auto sidx = [&](int row) { return (row ^ ((row >> PH::r) & 7)) * W + c; };
+  const ColIdx<PH, W> idx{c};
 
   // tile -> (instance, column block, operand): forward tiles alternate a / b
   auto decode = [&](int64_t tile, int64_t& inst, int64_t& cb, int& second) {
@@ -736,82 +648,23 @@ k_cols_tma(F fld, ColArgs<F> args, const __grid_constant__ CUtensorMap map0, con
     const T* tb_s = stage_buf + (size_t)st * ROWS * W;
 
     T x[R];
-    const int ph_first = INV ? NPH - 1 : 0;
-    {
-      const int rb = PH::ins_t(ph_first, t);
+    const int ph_in = INV ? NPH - 1 : 0, ph_out = INV ? 0 : NPH - 1;
 #pragma unroll
-      for (int s = 0; s < R; ++s) x[s] = tb_s[(rb + PH::cslot(ph_first, s)) * W + c];
-    }
-    if (!INV) {
-#pragma unroll
-      for (int ph = 0; ph < NPH; ++ph) {
-        if (ph > 0) {
-          const int wb = PH::ins_t(ph - 1, t);
-#pragma unroll
-          for (int s = 0; s < R; ++s) sm[sidx(wb + PH::cslot(ph - 1, s))] = x[s];
-          __syncthreads();
-          const int rb = PH::ins_t(ph, t);
-#pragma unroll
-          for (int s = 0; s < R; ++s) x[s] = sm[sidx(rb + PH::cslot(ph, s))];
-          __syncthreads();
-        }
-        const int rp = PH::rp(ph), lo = PH::lo(ph);
-        const int tb = (1 << K) | PH::ins_t(ph, t);
-#pragma unroll
-        for (int l = 0; l < rp; ++l) {
-          const int jb = rp - 1 - l;
-          const int bbit = lo + jb;
-          const int tsh = tb >> (bbit + 1);
-#pragma unroll
-          for (int s0 = 0; s0 < R; ++s0) {
-            if ((s0 >> jb) & 1) continue;
-            const int s1 = s0 + (1 << jb);
-            const Tw tw = args.twf[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
-            if (second) fld.fwd_b(x[s0], x[s1], tw);
-            else fld.fwd_a(x[s0], x[s1], tw);
-          }
-        }
-      }
-      const int rb = PH::ins_t(NPH - 1, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(NPH - 1, s)) * m] = x[s];
+    for (int s = 0; s < R; ++s) x[s] = tb_s[(PH::ins_t(ph_in, t) + PH::cslot(ph_in, s)) * W + c];
+    if constexpr (!INV) {
+      col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int row) {
+        const Tw tw = col_tw<K>(args.twf, bit, row);
+        if (second) fld.fwd_b(x[s0], x[s1], tw);
+        else fld.fwd_a(x[s0], x[s1], tw);
+      });
     } else {
-#pragma unroll
-      for (int ph = NPH - 1; ph >= 0; --ph) {
-        if (ph < NPH - 1) {
-          const int wb = PH::ins_t(ph + 1, t);
-#pragma unroll
-          for (int s = 0; s < R; ++s) sm[sidx(wb + PH::cslot(ph + 1, s))] = x[s];
-          __syncthreads();
-          const int rb = PH::ins_t(ph, t);
-#pragma unroll
-          for (int s = 0; s < R; ++s) x[s] = sm[sidx(rb + PH::cslot(ph, s))];
-          __syncthreads();
-        }
-        const int rp = PH::rp(ph), lo = PH::lo(ph);
-        const int tb = (1 << K) | PH::ins_t(ph, t);
-#pragma unroll
-        for (int l = 0; l < rp; ++l) {
-          const int jb = l;
-          const int bbit = lo + jb;
-          const int tsh = tb >> (bbit + 1);
-#pragma unroll
-          for (int s0 = 0; s0 < R; ++s0) {
-            if ((s0 >> jb) & 1) continue;
-            const int s1 = s0 + (1 << jb);
-            if (bbit == K - 1) {
-              fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
-            } else {
-              const Tw tw = args.twi[tsh | (PH::cslot(ph, s0) >> (bbit + 1))];
-              fld.inv(x[s0], x[s1], tw);
-            }
-          }
-        }
-      }
-      const int rb = PH::ins_t(0, t);
-#pragma unroll
-      for (int s = 0; s < R; ++s) dst[base + (int64_t)(rb + PH::cslot(0, s)) * m] = x[s];
+      col_inverse<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int row) {
+        if (bit == K - 1) fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
+        else fld.inv(x[s0], x[s1], col_tw<K>(args.twi, bit, row));
+      });
     }
+#pragma unroll
+    for (int s = 0; s < R; ++s) dst[base + (int64_t)(PH::ins_t(ph_out, t) + PH::cslot(ph_out, s)) * m] = x[s];
     __syncthreads();   // stage st and the exchange buffer are free for the next issue / tile
   }
 }
