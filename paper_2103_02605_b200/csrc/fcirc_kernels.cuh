@@ -193,6 +193,14 @@ __device__ __forceinline__ void inverse_phase(int ph, int t, BF bf) {
   }
 }
 
+// read-only twiddle load through the non-coherent (texture) path: the tables are immutable for the
+// lifetime of a plan, and the top levels of every phase are shared by many threads of a CTA
+__device__ __forceinline__ uint64_t ldtw(const uint64_t* p) { return __ldg(p); }
+__device__ __forceinline__ TwU32 ldtw(const TwU32* p) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  return TwU32{v.x, v.y};
+}
+
 // ------------------------------------------------------------------------------------------
 // k_block: fused sub-problem kernel
 // ------------------------------------------------------------------------------------------
@@ -266,11 +274,11 @@ k_block(F fld, BlockArgs<F> args) {
   // twiddle of the pair bit `bit` at address x: heap entry (2^k + E) 2^(M-1-bit) + (x >> (bit+1))
   auto twf_at = [&](int bit, int x) -> Tw {
     if constexpr (TWS) return twsf[tw_swz((1 << (M - 1 - bit)) - 1 + (x >> (bit + 1)))];
-    else return args.twf[(gbase | x) >> (bit + 1)];
+    else return ldtw(args.twf + ((gbase | x) >> (bit + 1)));
   };
   auto twi_at = [&](int bit, int x) -> Tw {
     if constexpr (TWS) return twsi[tw_swz((1 << (M - 1 - bit)) - 1 + (x >> (bit + 1)))];
-    else return args.twi[(gbase | x) >> (bit + 1)];
+    else return ldtw(args.twi + ((gbase | x) >> (bit + 1)));
   };
 
   T xa[R], xb[R];
@@ -370,7 +378,7 @@ struct ColIdx {
 // twiddles of the column levels: heap entry (2^K | row) >> (bit + 1), the same for every column
 template <int K, class Tw>
 __device__ __forceinline__ Tw col_tw(const Tw* table, int bit, int row) {
-  return table[((1 << K) | row) >> (bit + 1)];
+  return ldtw(table + (((1 << K) | row) >> (bit + 1)));
 }
 
 // The K forward levels of NG register arrays (same rows), NG in {1, 2}: bf runs the butterflies.
