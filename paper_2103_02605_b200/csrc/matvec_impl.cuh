@@ -82,11 +82,13 @@ static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t s
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
 
-// sub-problem launches (k > 0) of the 32-bit fields stage their twiddle slices in smem
+// The 32-bit fields stage their twiddle slices in smem for sub-problem launches (k > 0), and for
+// fused launches of a small batch (latency-bound: one coalesced table load per CTA instead of a
+// dependent L2 round trip per phase); large fused batches share the table through L1/L2 instead.
 template <class F, int M, int RR, bool EMB = false>
 static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
   if constexpr (TwStage<F, M>::value && !EMB)
-    if (args.k > 0) return launch_block_t<F, M, RR, false, true>(fld, args, st);
+    if (args.k > 0 || args.units <= 64) return launch_block_t<F, M, RR, false, true>(fld, args, st);
   return launch_block_t<F, M, RR, EMB, false>(fld, args, st);
 }
 
