@@ -372,8 +372,7 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
   const int64_t nseg = (nd + kCarrySeg - 1) / kCarrySeg;
-  const size_t need = (size_t)(3 * batch * L) * 4 + (size_t)(2 * batch * ncoef) * 8 + (size_t)(batch * nd) * 4 +
-                      (size_t)(batch * nseg) * 4;
+  const size_t need = (size_t)(3 * batch * L) * 4 + (size_t)(batch * nd) * 4 + (size_t)(batch * nseg) * 4;
   void* ws;
   int rc = ws_alloc(dev, st, need, &ws);
   if (rc) return rc;
@@ -381,11 +380,8 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   uint32_t* r1 = (uint32_t*)ws;
   uint32_t* r2 = r1 + batch * L;
   uint32_t* r3 = r2 + batch * L;
-  uint64_t* V = (uint64_t*)(r3 + batch * L);
-  uint32_t* E = (uint32_t*)(V + 2 * batch * ncoef);
+  uint32_t* E = r3 + batch * L;
   uint32_t* S = E + batch * nd;
-  const int thr = 256;
-  auto nblk = [&](int64_t tot) { return (unsigned)std::min<int64_t>((tot + thr - 1) / thr, 148 * 16); };
   // 16-bit limb split + a~ embedding fused into the first pass of each product (EMB_LIMBS)
   EmbedIO io;
   io.mode = EMB_LIMBS;
@@ -407,15 +403,7 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   g.c123 = (uint32_t)invmod(mulmod(P1 % P3, P2 % P3, P3), P3);
   g.c123q = (uint32_t)(((uint64_t)g.c123 << 32) / P3);
   prof_begin(4, st);
-  k_garner<<<nblk(batch * ncoef), thr, 0, st>>>(r1, r2, r3, L, ncoef, batch, g, V);
-  prof_end(st);
-  ++g_launches;
-  prof_begin(4, st);
-  k_digits<<<nblk(batch * nd), thr, 0, st>>>(V, ncoef, nd, batch, E);
-  prof_end(st);
-  ++g_launches;
-  prof_begin(4, st);
-  k_carry_seg<<<(unsigned)(batch * nseg), kCarryThreads, 0, st>>>(E, nd, nseg, S);
+  k_crt_digits<<<(unsigned)(batch * nseg), kCarryThreads, 0, st>>>(r1, r2, r3, L, ncoef, nd, nseg, g, E, S);
   prof_end(st);
   prof_begin(4, st);
   k_carry_top<<<(unsigned)batch, 32, 0, st>>>(S, nseg, batch);
@@ -423,7 +411,7 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   prof_begin(4, st);
   k_carry_apply<<<(unsigned)(batch * nseg), kCarryThreads, 0, st>>>(E, nd, nseg, S, z, nx + ny);
   prof_end(st);
-  g_launches += 3;
+  g_launches += 3;   // k_crt_digits, k_carry_top, k_carry_apply
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
 

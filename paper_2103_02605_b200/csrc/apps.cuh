@@ -3,7 +3,8 @@
 // The polynomial embedding (row a~, zero padding, truncation) and the big-integer limb
 // split are fused into the first / last pass of the product itself (fcirc_kernels.cuh EmbedIO).
 // What remains here is the tail of the big-integer product (reading R12):
-// Garner CRT of the three residues, 16-bit digit sums and the carry propagation.
+// Garner CRT of the three residues fused with the 16-bit digit sums and the per-segment carry
+// summary (k_crt_digits), then the carry propagation (k_carry_top, k_carry_apply).
 #pragma once
 #include <cstdint>
 
@@ -31,52 +32,26 @@ __device__ __forceinline__ uint32_t add_mod(uint32_t a, uint32_t b, uint32_t p) 
 
 // V_k = CRT(r1, r2, r3) for one coefficient (Garner, mixed radix p1, p1 p2):
 //   v1 = r1,  v2 = (r2 - v1) p1^-1 mod p2,  v3 = (r3 - v1 - v2 p1) (p1 p2)^-1 mod p3,
-//   V = v1 + v2 p1 + v3 p1 p2 < p1 p2 p3 < 2^85, stored as (low 64 bits, high bits).
+//   V = v1 + v2 p1 + v3 p1 p2 < p1 p2 p3 < 2^85, returned as (low 64 bits, high bits).
 // (Within bigint_mul's size limit every coefficient is < 2^54 < p1 p2, so v3 = 0; the general
 // three-prime reconstruction is kept as BASELINE.json's C5 route prescribes.)
-__global__ void k_garner(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2,
-                         const uint32_t* __restrict__ r3, int64_t L, int64_t ncoef, int64_t batch, GarnerConsts g,
-                         uint64_t* __restrict__ V) {
-  const int64_t tot = batch * ncoef;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t inst = i / ncoef, k = i - inst * ncoef;
-    const uint32_t v1 = r1[inst * L + k];
-    const uint32_t v2 = shoup_red(sub_mod(r2[inst * L + k], shoup_red(v1, 1u, g.one2q, g.p2), g.p2), g.c12, g.c12q, g.p2);
-    const uint32_t t = add_mod(shoup_red(v1, 1u, g.one3q, g.p3), shoup_red(v2, g.p1m3, g.p1m3q, g.p3), g.p3);
-    const uint32_t v3 = shoup_red(sub_mod(r3[inst * L + k], t, g.p3), g.c123, g.c123q, g.p3);
-    const unsigned __int128 val = (unsigned __int128)v1 + (unsigned __int128)v2 * g.p1 +
-                                  (unsigned __int128)v3 * g.p1p2;
-    V[2 * i] = (uint64_t)val;
-    V[2 * i + 1] = (uint64_t)(val >> 64);
-  }
-}
-
-__device__ __forceinline__ uint32_t chunk16(const uint64_t* V, int64_t k, int i) {
-  return (uint32_t)(V[2 * k + (i >> 2)] >> (16 * (i & 3))) & 0xFFFFu;
-}
-
-// D_j = sum_{i<6} chunk_i(V_{j-i})  (< 6 * 2^16);  E_j = (D_j mod 2^16) + floor(D_{j-1} / 2^16)  (< 2^16 + 6)
-__global__ void k_digits(const uint64_t* __restrict__ V, int64_t ncoef, int64_t nd, int64_t batch,
-                         uint32_t* __restrict__ Eo) {
-  const int64_t tot = batch * nd;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t inst = i / nd, j = i - inst * nd;
-    const uint64_t* Vi = V + 2 * inst * ncoef;
-    uint32_t D = 0, Dm = 0;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-      if (j - q >= 0 && j - q < ncoef) D += chunk16(Vi, j - q, q);
-      if (j - 1 - q >= 0 && j - 1 - q < ncoef) Dm += chunk16(Vi, j - 1 - q, q);
-    }
-    Eo[i] = (D & 0xFFFFu) + (Dm >> 16);
-  }
+__device__ __forceinline__ void garner(uint32_t r1, uint32_t r2, uint32_t r3, const GarnerConsts& g, uint64_t& lo,
+                                       uint64_t& hi) {
+  const uint32_t v1 = r1;
+  const uint32_t v2 = shoup_red(sub_mod(r2, shoup_red(v1, 1u, g.one2q, g.p2), g.p2), g.c12, g.c12q, g.p2);
+  const uint32_t t = add_mod(shoup_red(v1, 1u, g.one3q, g.p3), shoup_red(v2, g.p1m3, g.p1m3q, g.p3), g.p3);
+  const uint32_t v3 = shoup_red(sub_mod(r3, t, g.p3), g.c123, g.c123q, g.p3);
+  const unsigned __int128 val = (unsigned __int128)v1 + (unsigned __int128)v2 * g.p1 +
+                                (unsigned __int128)v3 * g.p1p2;
+  lo = (uint64_t)val;
+  hi = (uint64_t)(val >> 64);
 }
 
 // ------------------------------------------------------------------------------------------
 // carry propagation: E_j = e_j + g_j 2^16 with g_j in {0, 1}; digit j absorbs the carry c_j,
 // c_{j+1} = g_j | (p_j & c_j), p_j = (e_j == 0xFFFF).  (G, P) pairs compose associatively
 // (earlier segment X, later Y): (G_Y | (P_Y & G_X), P_Y & P_X).  Three launches:
-//   k_carry_seg   per (integer, segment of kCarrySeg digits): the segment's (G, P)
+//   k_crt_digits  per (integer, segment of kCarrySeg digits): CRT, digits and the segment's (G, P)
 //   k_carry_top   per integer: exclusive scan over its segments -> carry into each segment
 //   k_carry_apply per (integer, segment): block scan with the carry-in, write 32-bit words
 // Each thread owns kCarryPer consecutive digits (coalesced uint4 loads).
@@ -122,12 +97,46 @@ __device__ __forceinline__ GP local_gp(const uint32_t e[kCarryPer]) {
   return acc;
 }
 
+// One CTA per (integer, segment of kCarrySeg digits): Garner CRT of the coefficients the segment
+// needs (its own and 6 below it) into shared memory, the digits
+//   D_j = sum_{i<6} chunk16_i(V_{j-i}) (< 6 * 2^16),  E_j = (D_j mod 2^16) + floor(D_{j-1} / 2^16)
+// (< 2^16 + 6, so every carry is 0 or 1), written to E for the final pass, and the segment's
+// carry-lookahead pair (G, P) -- one launch instead of CRT, digit and segment kernels, and no
+// 128-bit coefficient array in global memory.
+constexpr int kHalo = 6;
 __global__ void __launch_bounds__(kCarryThreads)
-k_carry_seg(const uint32_t* __restrict__ E, int64_t nd, int64_t nseg, uint32_t* __restrict__ seg_gp) {
+k_crt_digits(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2, const uint32_t* __restrict__ r3,
+             int64_t L, int64_t ncoef, int64_t nd, int64_t nseg, GarnerConsts g, uint32_t* __restrict__ E,
+             uint32_t* __restrict__ seg_gp) {
+  __shared__ uint16_t ch[kCarrySeg + kHalo][6];   // 16-bit chunks of V_k, k = j0 - kHalo + row
   const int64_t inst = blockIdx.x / nseg, sg = blockIdx.x - inst * nseg;
-  const int64_t j0 = sg * kCarrySeg + (int64_t)threadIdx.x * kCarryPer;
+  const int64_t j0 = sg * kCarrySeg;
+  const uint32_t *a1 = r1 + inst * L, *a2 = r2 + inst * L, *a3 = r3 + inst * L;
+  for (int q = threadIdx.x; q < kCarrySeg + kHalo; q += kCarryThreads) {
+    const int64_t k = j0 - kHalo + q;
+    uint64_t lo = 0, hi = 0;
+    if (k >= 0 && k < ncoef) garner(a1[k], a2[k], a3[k], g, lo, hi);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) ch[q][i] = (uint16_t)((i < 4 ? lo >> (16 * i) : hi >> (16 * (i - 4))) & 0xFFFFu);
+  }
+  __syncthreads();
   uint32_t e[kCarryPer];
-  load_digits(E + inst * nd, nd, j0, e);
+  const int jl0 = threadIdx.x * kCarryPer;   // local digit index
+#pragma unroll
+  for (int d = 0; d < kCarryPer; ++d) {
+    const int jl = jl0 + d;                  // digit j = j0 + jl uses rows jl + kHalo - i
+    uint32_t D = 0, Dm = 0;
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      D += ch[jl + kHalo - i][i];
+      Dm += ch[jl + kHalo - 1 - i][i];
+    }
+    e[d] = (j0 + jl < nd) ? (D & 0xFFFFu) + (Dm >> 16) : 0u;
+  }
+  uint32_t* Ei = E + inst * nd;
+#pragma unroll
+  for (int d = 0; d < kCarryPer; ++d)
+    if (j0 + jl0 + d < nd) Ei[j0 + jl0 + d] = e[d];
   GP tot;
   gp_block_exscan(local_gp(e), &tot);
   if (threadIdx.x == 0) seg_gp[blockIdx.x] = tot.g | (tot.p << 1);

@@ -602,7 +602,7 @@ k_cols_tma(F fld, ColArgs<F> args, const __grid_constant__ CUtensorMap map0, con
   constexpr uint32_t TILE_BYTES = (uint32_t)(ROWS * W * sizeof(T));
   // dynamic smem only (a static __shared__ variable would shift the dynamic base off the 128-byte
   // alignment TMA destinations need): [stage 0][stage 1][exchange][2 mbarriers]
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   // round the base up to 128 bytes in the shared window (the launch adds 128 bytes of slack)
   const uint32_t raw = smem_u32(smem_raw);
   T* stage_buf = reinterpret_cast<T*>(smem_raw + (((raw + 127u) & ~127u) - raw));  // 2 x [ROWS][W] dense
