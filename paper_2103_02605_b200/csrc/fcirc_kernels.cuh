@@ -129,8 +129,10 @@ __device__ __forceinline__ void io_store(T* dst, int64_t inst, int64_t pos, int6
 //                         phase ph_from to that of ph_to through shared memory; idx(base, slot)
 //                         maps an address (k_block: position, k_cols: row) given as its thread
 //                         part plus its compile-time slot part to the swizzled smem index
-//   forward_phase         the split levels of phase ph, top address bit first: bf(s0, s1, bit, x)
+//   forward_phase         the split levels of phase ph, top address bit first: bf(s0, s1, bit, tb, cs)
 //                         gets the two slots of a butterfly pair, the pair bit and the address
+//                         tb | cs of slot s0 split into its thread part tb and its compile-time
+//                         slot part cs (disjoint bits), so twiddle indices separate the same way
 //   inverse_phase         the recombination levels of phase ph, low address bit first
 // All loops are fully unrolled (compile-time slots), so the register arrays stay in registers.
 // ------------------------------------------------------------------------------------------
@@ -175,7 +177,7 @@ __device__ __forceinline__ void forward_phase(int ph, int t, BF bf) {
 #pragma unroll
     for (int s0 = 0; s0 < R; ++s0) {
       if ((s0 >> jb) & 1) continue;
-      bf(s0, s0 + (1 << jb), lo + jb, tins | PH::cslot(ph, s0));
+      bf(s0, s0 + (1 << jb), lo + jb, tins, PH::cslot(ph, s0));
     }
   }
 }
@@ -188,7 +190,7 @@ __device__ __forceinline__ void inverse_phase(int ph, int t, BF bf) {
 #pragma unroll
     for (int s0 = 0; s0 < R; ++s0) {
       if ((s0 >> jb) & 1) continue;
-      bf(s0, s0 + (1 << jb), lo + jb, tins | PH::cslot(ph, s0));
+      bf(s0, s0 + (1 << jb), lo + jb, tins, PH::cslot(ph, s0));
     }
   }
 }
@@ -255,30 +257,28 @@ k_block(F fld, BlockArgs<F> args) {
 
   // Twiddle staging (32-bit fields): the CTA's sub-block uses the heap slice
   // {2^(k+j) + E 2^j + e' : j < M, e' < 2^j} of each table (contiguous per level).
-  // It is copied once, coalesced, into shared memory at local heap index 2^j - 1 + e', so the
+  // It is copied once, coalesced, into shared memory at local heap index 2^j + e' (1-based), so the
   // butterflies read twiddles with LDS instead of scattered L2 loads (profiles/r01c: the u32
   // k_block stalled on long_scoreboard).  Goldilocks is arithmetic-bound and keeps the LDG path;
   // so does the fused whole-product launch (k = 0), whose CTAs all share one table via L1/L2.
   Tw* twsf = reinterpret_cast<Tw*>(sm + (size_t)IPC * 2 * m);
   Tw* twsi = twsf + m;
   if constexpr (TWS) {
-    for (int q = threadIdx.x; q < m - 1; q += blockDim.x) {
-      const int j = 31 - __clz(q + 1);
-      const int e = q + 1 - (1 << j);
-      const int g = (1 << (k + j)) + (E << j) + e;
-      twsf[tw_swz(q)] = args.twf[g];
-      twsi[tw_swz(q)] = args.twi[g];
+    for (int h = threadIdx.x + 1; h < m; h += blockDim.x) {
+      const int j = 31 - __clz(h);
+      const int g = (1 << (k + j)) + (E << j) + (h - (1 << j));
+      twsf[tw_swz(h)] = args.twf[g];
+      twsi[tw_swz(h)] = args.twi[g];
     }
     __syncthreads();
   }
-  // twiddle of the pair bit `bit` at address x: heap entry (2^k + E) 2^(M-1-bit) + (x >> (bit+1))
-  auto twf_at = [&](int bit, int x) -> Tw {
-    if constexpr (TWS) return twsf[tw_swz((1 << (M - 1 - bit)) - 1 + (x >> (bit + 1)))];
-    else return ldtw(args.twf + ((gbase | x) >> (bit + 1)));
-  };
-  auto twi_at = [&](int bit, int x) -> Tw {
-    if constexpr (TWS) return twsi[tw_swz((1 << (M - 1 - bit)) - 1 + (x >> (bit + 1)))];
-    else return ldtw(args.twi + ((gbase | x) >> (bit + 1)));
+  // twiddle of the pair bit `bit` at address x = tb | cs: heap entry (gbase | x) >> (bit+1), whose
+  // thread part (gbase | tb) >> (bit+1) is shared by every slot of a level and whose slot part
+  // cs >> (bit+1) is a compile-time offset (disjoint bits: the sum is the OR).  Staged: local heap
+  // index 2^(M-1-bit) | (x >> (bit+1)), swizzled with the GF(2)-linear tw_swz term by term.
+  auto tw_at = [&](const Tw* table, const Tw* staged, int bit, int tb, int cs) -> Tw {
+    if constexpr (TWS) return staged[tw_swz(1 << (M - 1 - bit)) ^ tw_swz(tb >> (bit + 1)) ^ tw_swz(cs >> (bit + 1))];
+    else return ldtw(table + ((gbase | tb) >> (bit + 1)) + (cs >> (bit + 1)));
   };
 
   T xa[R], xb[R];
@@ -304,8 +304,8 @@ k_block(F fld, BlockArgs<F> args) {
 #pragma unroll
   for (int ph = 0; ph < NPH; ++ph) {
     if (ph > 0) exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx);
-    forward_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int x) {
-      const Tw tw = twf_at(bit, x);
+    forward_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
+      const Tw tw = tw_at(args.twf, twsf, bit, tb, cs);
       fld.fwd_a(xa[s0], xa[s1], tw);
       fld.fwd_b(xb[s0], xb[s1], tw);
     });
@@ -328,9 +328,9 @@ k_block(F fld, BlockArgs<F> args) {
 #pragma unroll
     for (int ph = NPH - 1; ph >= 0; --ph) {
       if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx);
-      inverse_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int x) {
+      inverse_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
         if (bit == M - 1 && top) fld.inv_last(xm[s0], xm[s1], args.last_si, args.last_k);
-        else fld.inv(xm[s0], xm[s1], twi_at(bit, x));
+        else fld.inv(xm[s0], xm[s1], tw_at(args.twi, twsi, bit, tb, cs));
       });
     }
 
@@ -375,10 +375,11 @@ struct ColIdx {
   __device__ __forceinline__ int operator()(int base_part, int slot_part) const { return (*this)(base_part + slot_part); }
 };
 
-// twiddles of the column levels: heap entry (2^K | row) >> (bit + 1), the same for every column
+// twiddles of the column levels: heap entry (2^K | row) >> (bit + 1), the same for every column;
+// row = tb | cs (thread part, compile-time slot part; disjoint bits) as in k_block
 template <int K, class Tw>
-__device__ __forceinline__ Tw col_tw(const Tw* table, int bit, int row) {
-  return ldtw(table + (((1 << K) | row) >> (bit + 1)));
+__device__ __forceinline__ Tw col_tw(const Tw* table, int bit, int tb, int cs) {
+  return ldtw(table + (((1 << K) | tb) >> (bit + 1)) + (cs >> (bit + 1)));
 }
 
 // The K forward levels of NG register arrays (same rows), NG in {1, 2}: bf runs the butterflies.
@@ -437,15 +438,15 @@ k_cols(F fld, ColArgs<F> args) {
     else x[s] = src[base + row * m];
   }
   if constexpr (!INV) {
-    col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int row) {
-      const Tw tw = col_tw<K>(args.twf, bit, row);
+    col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
+      const Tw tw = col_tw<K>(args.twf, bit, tb, cs);
       if (second) fld.fwd_b(x[s0], x[s1], tw);
       else fld.fwd_a(x[s0], x[s1], tw);
     });
   } else {
-    col_inverse<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int row) {
+    col_inverse<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
       if (bit == K - 1) fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
-      else fld.inv(x[s0], x[s1], col_tw<K>(args.twi, bit, row));
+      else fld.inv(x[s0], x[s1], col_tw<K>(args.twi, bit, tb, cs));
     });
   }
 #pragma unroll
@@ -493,8 +494,8 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
       xb[s] = args.src1[base + row * m];
     }
   }
-  col_forward<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int row) {
-    const Tw tw = col_tw<K>(args.twf, bit, row);
+  col_forward<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
+    const Tw tw = col_tw<K>(args.twf, bit, tb, cs);
     fld.fwd_a(xa[s0], xa[s1], tw);
     fld.fwd_b(xb[s0], xb[s1], tw);
   });
@@ -535,12 +536,12 @@ k_cols_inv2(F fld, ColArgs<F> args) {
     xa[s] = args.src0[ad];
     xb[s] = args.src0[ad + W];
   }
-  col_inverse<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int row) {
+  col_inverse<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
     if (bit == K - 1) {
       fld.inv_last(xa[s0], xa[s1], args.last_si, args.last_k);
       fld.inv_last(xb[s0], xb[s1], args.last_si, args.last_k);
     } else {
-      const Tw tw = col_tw<K>(args.twi, bit, row);
+      const Tw tw = col_tw<K>(args.twi, bit, tb, cs);
       fld.inv(xa[s0], xa[s1], tw);
       fld.inv(xb[s0], xb[s1], tw);
     }
@@ -660,15 +661,15 @@ k_cols_tma(F fld, ColArgs<F> args, const __grid_constant__ CUtensorMap map0, con
 #pragma unroll
     for (int s = 0; s < R; ++s) x[s] = tb_s[(PH::ins_t(ph_in, t) + PH::cslot(ph_in, s)) * W + c];
     if constexpr (!INV) {
-      col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int row) {
-        const Tw tw = col_tw<K>(args.twf, bit, row);
+      col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
+        const Tw tw = col_tw<K>(args.twf, bit, tb, cs);
         if (second) fld.fwd_b(x[s0], x[s1], tw);
         else fld.fwd_a(x[s0], x[s1], tw);
       });
     } else {
-      col_inverse<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int row) {
+      col_inverse<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
         if (bit == K - 1) fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
-        else fld.inv(x[s0], x[s1], col_tw<K>(args.twi, bit, row));
+        else fld.inv(x[s0], x[s1], col_tw<K>(args.twi, bit, tb, cs));
       });
     }
 #pragma unroll
