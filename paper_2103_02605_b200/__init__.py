@@ -38,7 +38,8 @@ def fp2_pack(u: int, v: int) -> int:
     return (int(u) % M31X2) | ((int(v) % M31X2) << 32)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "lib", "libfcirc.so")
+# FCIRC_LIB: an alternative build of the same library (A/B experiments, tools/gpu_sweep.sh)
+_LIB_PATH = os.environ.get("FCIRC_LIB") or os.path.join(_HERE, "lib", "libfcirc.so")
 _lib = None
 
 
