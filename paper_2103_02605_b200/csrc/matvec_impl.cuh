@@ -24,6 +24,7 @@ template <> struct FTraits<FieldU32> {
   static constexpr int MMAX = 13;   // 2 x 2^13 x 4 B data + 2 x 2^13 x 8 B staged twiddles = 192 KB smem
   static constexpr int MPREF = 12;  // 96 KB: two CTAs per SM
   static constexpr const char* RB = "U32_RB";
+  static constexpr const char* RBF = "U32_RBF";
   static constexpr const char* RC = "U32_RC";
   static constexpr const char* MS = "U32_MSPLIT";
   static constexpr int TMA_MIN_K = 9;   // TMA inverse column passes from this depth on; below it
@@ -33,6 +34,7 @@ template <> struct FTraits<FieldGold> {
   static constexpr int MMAX = 13;   // 2 x 2^13 x 8 B = 128 KB smem per sub-problem
   static constexpr int MPREF = 12;  // 64 KB: two CTAs per SM
   static constexpr const char* RB = "GOLD_RB";
+  static constexpr const char* RBF = "GOLD_RBF";
   static constexpr const char* RC = "GOLD_RC";
   static constexpr const char* MS = "GOLD_MSPLIT";
   static constexpr int TMA_MIN_K = 9;
@@ -41,6 +43,7 @@ template <> struct FTraits<FieldM31x2> {      // the paper's ring, 8-byte packed
   static constexpr int MMAX = 13;
   static constexpr int MPREF = 12;
   static constexpr const char* RB = "M31_RB";
+  static constexpr const char* RBF = "M31_RBF";
   static constexpr const char* RC = "M31_RC";
   static constexpr const char* MS = "M31_MSPLIT";
   static constexpr int TMA_MIN_K = 9;
@@ -64,9 +67,13 @@ static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t s
   using E = typename F::T;
   constexpr int PM = 1 << M;  // swizzled, unpadded (fcirc_kernels.cuh swz)
   const size_t smem = (size_t)IPC * 2 * PM * sizeof(E) + (TWS ? (size_t)2 * (1 << M) * sizeof(typename F::Tw) : 0);
-  // occupancy target: 1024 resident threads per SM for R <= 8 (register cap 64), 512 for R = 16
-  // (cap 128: without a floor ptxas spends ~190 registers and halves the resident warps)
-  constexpr int MINB = (T * IPC < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / (T * IPC) : 1;
+  // occupancy target: 1024 resident threads per SM (register cap 64) for R <= 8, and for R = 16
+  // with 32-bit elements when the twiddles are not staged (plain loads, M = 12: fits 64 registers
+  // with at most a 16-byte spill; measured C2 +5.6 %, profiles/r01h_sweep_u32_r16.txt); 512 otherwise (cap 128: without a floor ptxas spends ~190
+  // registers and halves the resident warps; with staged twiddles shared memory admits only two
+  // 256-thread CTAs per SM anyway, and a 64-register cap would only add spills)
+  constexpr int TGT = (RR <= 8 || (sizeof(E) == 4 && !TWS && !EMB && M == 12)) ? 1024 : 512;
+  constexpr int MINB = (T * IPC < TGT) ? TGT / (T * IPC) : 1;
   auto kern = k_block<F, M, R, IPC, MINB, EMB, TWS>;
   // opt-in shared memory, once per instantiation (thread-safe static initialisation)
   static const bool attr_ok =
@@ -229,16 +236,22 @@ static int launch_cols_tma(const F& fld, ColArgs<F> args, int64_t instances, cud
 // Smaller R = more threads per sub-problem and fewer registers per thread: more resident warps to
 // hide the latency of the carry chains, at the price of more shared-memory exchange phases.
 template <class F> struct RDefault;
-template <> struct RDefault<FieldU32> { static constexpr int RB = 8, RC = 16; };
-template <> struct RDefault<FieldGold> { static constexpr int RB = 8, RC = 8; };
-template <> struct RDefault<FieldM31x2> { static constexpr int RB = 8, RC = 8; };
+// RB: sub-problem launches (and the staged-twiddle small fused ones); RBF: fused launches of a large
+// batch with plain twiddle loads (u32: R = 16 at 1024 threads/SM, C2 +5 %; the staged sub-problem
+// kernels measured 0.1-0.5 % faster with R = 8, profiles/r01h_sweep_u32_r16.txt)
+template <> struct RDefault<FieldU32> { static constexpr int RB = 8, RBF = 16, RC = 16; };
+template <> struct RDefault<FieldGold> { static constexpr int RB = 8, RBF = 8, RC = 8; };
+template <> struct RDefault<FieldM31x2> { static constexpr int RB = 8, RBF = 8, RC = 8; };
 
 template <class F, int M>
 static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
   // the application embeddings (fused path only) use one variant: the default R
   if (args.k == 0 && args.io.mode != EMB_PLAIN) return launch_block<F, M, RDefault<F>::RB, true>(fld, args, st);
   if constexpr (M >= FTraits<F>::MMAX - 2) {
-    static const int r = knob(FTraits<F>::RB, RDefault<F>::RB);
+    static const int rb = knob(FTraits<F>::RB, RDefault<F>::RB);
+    static const int rbf = knob(FTraits<F>::RBF, RDefault<F>::RBF);
+    const bool fused_plain = args.k == 0 && !(TwStage<F, M>::value && args.units <= 64);
+    const int r = fused_plain ? rbf : rb;
     if (r == 8) return launch_block<F, M, 8>(fld, args, st);
     if constexpr ((1 << M) / 4 <= 1024)  // one sub-problem per CTA: at most 1024 threads
       if (r == 4) return launch_block<F, M, 4>(fld, args, st);
