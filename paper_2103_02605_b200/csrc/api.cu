@@ -323,7 +323,8 @@ static std::map<int, HostCtx> g_host;
 static int host_pipeline(uint64_t p, uint64_t f, const char* a, const char* b, char* c, int64_t n, int64_t batch,
                          size_t es, int dev) {
   const size_t inst_bytes = (size_t)n * es;
-  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(batch, (int64_t)((size_t)32 << 20) / (int64_t)inst_bytes));
+  static const int64_t chunk_mb = std::max(1, knob("HOST_CHUNK_MB", 32));  // per operand and chunk
+  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(batch, (chunk_mb << 20) / (int64_t)inst_bytes));
   const size_t slot_bytes = 3 * (size_t)C * inst_bytes;
   std::lock_guard<std::mutex> lk(g_host_mu);
   HostCtx& hc = g_host[dev];

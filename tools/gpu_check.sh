@@ -23,4 +23,20 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ -
 timeout 300 python bench.py --config S1 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain_s1.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ -s 3 -c 3 -o gpurun_out/prof_${TAG}_S1 \
   python bench.py --config S1 --steps 2 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu3.log 2>&1
+# gpurun copies back at most 64 MiB of gpurun_out/: summarise the reports here and keep only the
+# text summaries, the raw metric CSVs and the traffic table (the .ncu-rep files are ~20-50 MB each)
+cp profiles/traffic.json gpurun_out/traffic.json
+[ -f gpurun_out/launches_$TAG.csv ] && python tools/ncu_summary.py launches gpurun_out/launches_$TAG.csv > gpurun_out/launches_$TAG.txt
+if [ -f gpurun_out/prof_$TAG.ncu-rep ]; then
+  python tools/ncu_summary.py traffic gpurun_out/prof_$TAG.ncu-rep k_block_sub C4_n20 "k_block" gpurun_out/traffic.json
+fi
+if [ -f gpurun_out/prof_${TAG}_S1.ncu-rep ]; then
+  python tools/ncu_summary.py traffic gpurun_out/prof_${TAG}_S1.ncu-rep k_block_sub S1 "k_block" gpurun_out/traffic.json
+fi
+for r in gpurun_out/prof_$TAG.ncu-rep gpurun_out/prof_${TAG}_S1.ncu-rep; do
+  [ -f $r ] || continue
+  python tools/ncu_summary.py full $r > ${r%.ncu-rep}_full.txt
+  ncu -i $r --page raw --csv > ${r%.ncu-rep}_raw.csv 2>/dev/null
+  rm -f $r
+done
 echo done
