@@ -136,6 +136,11 @@ __device__ __forceinline__ void io_store(T* dst, int64_t inst, int64_t pos, int6
 //   inverse_phase         the recombination levels of phase ph, low address bit first
 // All loops are fully unrolled (compile-time slots), so the register arrays stay in registers.
 // ------------------------------------------------------------------------------------------
+// One barrier per exchange (read-after-write).  No barrier is needed between an exchange's reads
+// and the next exchange's writes to the same buffer: a thread reads the addresses of the slots it
+// holds in phase ph_to and the next exchange (from ph_to) writes exactly those addresses, so it
+// only overwrites values it has already read itself.  Callers that reuse the buffer with another
+// layout (k_cols_tma between tiles) synchronise themselves.
 template <class PH, int R, class T, class Idx>
 __device__ __forceinline__ void exchange(T (&x)[R], T* buf, int ph_from, int ph_to, int t, Idx idx) {
   const int wb = PH::ins_t(ph_from, t);
@@ -145,7 +150,6 @@ __device__ __forceinline__ void exchange(T (&x)[R], T* buf, int ph_from, int ph_
   const int rb = PH::ins_t(ph_to, t);
 #pragma unroll
   for (int s = 0; s < R; ++s) x[s] = buf[idx(rb, PH::cslot(ph_to, s))];
-  __syncthreads();
 }
 
 template <class PH, int R, class T, class Idx>
@@ -165,7 +169,6 @@ __device__ __forceinline__ void exchange2(T (&x)[R], T (&y)[R], T* bx, T* by, in
     x[s] = bx[ad];
     y[s] = by[ad];
   }
-  __syncthreads();
 }
 
 template <class PH, int R, class BF>
