@@ -198,6 +198,17 @@ __device__ __forceinline__ void inverse_phase(int ph, int t, BF bf) {
   }
 }
 
+// Instance base pointer as an opaque value: element accesses p[off] with a 32-bit row offset then
+// compile to one IMAD.WIDE.U32 (off * sizeof(T) + p) instead of a re-associated 64-bit index
+// computation (shift, add, add-with-carry).  Used where it measured faster: the Goldilocks forward
+// column pass (-3 %; the u32 column passes and the TMA inverse measured 2-9 % slower with it,
+// profiles/r01i_sweep_col_offsets_ab.txt).
+template <class P>
+__device__ __forceinline__ P* opaque(P* p) {
+  asm("" : "+l"(p));
+  return p;
+}
+
 // read-only twiddle load through the non-coherent (texture) path: the tables are immutable for the
 // lifetime of a plan, and the top levels of every phase are shared by many threads of a CTA
 __device__ __forceinline__ uint64_t ldtw(const uint64_t* p) { return __ldg(p); }
@@ -485,6 +496,10 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
   const int64_t m = args.m;
   const ColIdx<PH, W> idx{c};
 
+  constexpr bool OFF32 = sizeof(T) == 8;   // 32-bit row offsets (row m < n <= 2^24) from opaque bases
+  const uint32_t mm = (uint32_t)m;
+  const T* pa = opaque(args.src0 + base);
+  const T* pb = opaque(args.src1 + base);
   T xa[R], xb[R];
 #pragma unroll
   for (int s = 0; s < R; ++s) {
@@ -492,6 +507,9 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
     if constexpr (EMB) {
       xa[s] = io_load(args.src0, inst, col + row * m, args.n, false, args.io);
       xb[s] = io_load(args.src1, inst, col + row * m, args.n, true, args.io);
+    } else if constexpr (OFF32) {
+      xa[s] = pa[(uint32_t)row * mm];
+      xb[s] = pb[(uint32_t)row * mm];
     } else {
       xa[s] = args.src0[base + row * m];
       xb[s] = args.src1[base + row * m];
@@ -502,11 +520,19 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
     fld.fwd_a(xa[s0], xa[s1], tw);
     fld.fwd_b(xb[s0], xb[s1], tw);
   });
+  T* qa = opaque(args.dst0 + base);
+  T* qb = opaque(args.dst1 + base);
 #pragma unroll
   for (int s = 0; s < R; ++s) {
-    const int64_t ad = base + (int64_t)(PH::ins_t(NPH - 1, t) + PH::cslot(NPH - 1, s)) * m;
-    args.dst0[ad] = xa[s];
-    args.dst1[ad] = xb[s];
+    if constexpr (OFF32) {
+      const uint32_t ad = (uint32_t)(PH::ins_t(NPH - 1, t) + PH::cslot(NPH - 1, s)) * mm;
+      qa[ad] = xa[s];
+      qb[ad] = xb[s];
+    } else {
+      const int64_t ad = base + (int64_t)(PH::ins_t(NPH - 1, t) + PH::cslot(NPH - 1, s)) * m;
+      args.dst0[ad] = xa[s];
+      args.dst1[ad] = xb[s];
+    }
   }
 }
 
