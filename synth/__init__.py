@@ -64,6 +64,20 @@ def uniform(rng: np.random.Generator, p: int, shape) -> np.ndarray:
     return rng.integers(0, p, size=shape, dtype=np.uint64).astype(dtype_for(p))
 
 
+def edge_mix(p: int, shape, rng) -> np.ndarray:
+    """Residues in [0, p) biased to the carry/borrow corner cases of the kernels' arithmetic: half of
+    the entries from {0, 1, 2, p-1, p-2, 2^31 +- 1, 2^32 +- 1, 2^63, p - 2^32, ...} (those < p),
+    half uniform.  No arithmetic of the method (value generation only)."""
+    cand = [0, 1, 2, p - 1, p - 2, p - 3, (1 << 31) - 1, 1 << 31, (1 << 31) + 1, (1 << 32) - 1, 1 << 32,
+            (1 << 32) + 1, (1 << 63) - 1, 1 << 63, (1 << 64) - (1 << 33), p - (1 << 32), p - (1 << 32) + 1,
+            (p - 1) // 2, (p + 1) // 2]
+    edges = np.array(sorted({c for c in cand if 0 <= c < p}), dtype=np.uint64)
+    pick = edges[rng.integers(0, len(edges), size=shape)]
+    unif = rng.integers(0, p, size=shape, dtype=np.uint64)
+    out = np.where(rng.integers(0, 2, size=shape) == 1, pick, unif)
+    return out.astype(np.uint32 if p < (1 << 32) else np.uint64)
+
+
 def matvec_inputs(p: int, n: int, batch: int, seed: int, f_mode: str = "wn"):
     """Inputs of one f-circulant matvec run.
 

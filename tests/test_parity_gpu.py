@@ -115,6 +115,24 @@ def test_matvec_extreme_values():
                     check_sampled(inp, c, [0], count=256, thetas=0)
 
 
+@pytest.mark.parametrize("p", PRIMES)
+def test_matvec_edge_value_mix(p):
+    """Inputs biased to the carry / borrow / canonicalisation corners (synth.edge_mix: p-1, p-2,
+    2^32 +- 1, 2^63, p - 2^32, ...): every entry through the fused (n <= 2^12) and the three-pass
+    (2^13) schedules, sampled entries + checksum at 2^16."""
+    rng = np.random.default_rng(4242 + p % 1000)
+    for L in [10, 12, 13, 16]:
+        n = 1 << L
+        w = int(rng.integers(1, p, dtype=np.uint64))
+        inp = dict(p=p, n=n, batch=2, f=pow(w, n, p), w=w,
+                   a=synth.edge_mix(p, (2, n), rng), b=synth.edge_mix(p, (2, n), rng))
+        c = run_matvec(inp)
+        if L <= 13:
+            check_full(inp, c)
+        else:
+            check_sampled(inp, c, [0, 1], count=512, thetas=2)
+
+
 # ---------------------------------------------------------------------------------- multi-pass
 
 @pytest.mark.parametrize("p", PRIMES)
