@@ -257,6 +257,17 @@ def test_polymul_small_full(p):
             assert np.array_equal(c[k].astype(np.uint64), exp), (na, nb, k)
 
 
+@pytest.mark.parametrize("p", [P998, GOLDILOCKS])
+def test_polymul_edge_value_mix(p):
+    """Polynomial products on corner-biased coefficients (synth.edge_mix), fused and multi-pass."""
+    rng = np.random.default_rng(99)
+    for na, nb in [(100, 77), (3000, 2000), (9000, 7000)]:
+        a, b = synth.edge_mix(p, (2, na), rng), synth.edge_mix(p, (2, nb), rng)
+        c = _host(fc.polymul(_dev(a), _dev(b), p))
+        for k in range(2):
+            assert np.array_equal(c[k].astype(np.uint64), oracle.polymul_coeffs(p, a[k], b[k])), (na, nb, k)
+
+
 def test_config_C3_polymul():
     cfg = synth.CONFIGS["C3"]
     inp = synth.polymul_inputs(cfg["p"], cfg["na"], cfg["nb"], cfg["batch"], cfg["seed"])
@@ -414,6 +425,25 @@ def test_m31x2_matvec_all_entries(f_mode):
             exp = oracle.fcirc_entries_m31x2(inp["f"], inp["a"][k], inp["b"][k])
             got = c[k].astype(np.uint64)
             bad = np.nonzero(got != exp)[0]
+            assert bad.size == 0, (L, k, bad[:4])
+
+
+def test_m31x2_matvec_edge_components():
+    """Z/(2^31-1)[sqrt 3] with both components drawn from the corner set (0, 1, p-1, p-2, 2^30, ...):
+    the per-component folds of FieldM31x2 at their extremes, every entry, fused and multi-pass."""
+    rng = np.random.default_rng(31)
+    p = (1 << 31) - 1
+    for L in [6, 12, 13]:
+        n = 1 << L
+        u = synth.edge_mix(p, (2, 2, n), rng).astype(np.uint64)
+        a = (u[0] | (synth.edge_mix(p, (2, n), rng).astype(np.uint64) << np.uint64(32)))
+        b = (u[1] | (synth.edge_mix(p, (2, n), rng).astype(np.uint64) << np.uint64(32)))
+        base = synth.matvec_inputs(M31X2, n, 1, seed=700 + L)
+        inp = dict(p=M31X2, n=n, batch=2, f=base["f"], w=base["w"], a=a, b=b)
+        c = run_matvec(inp)
+        for k in range(2):
+            exp = oracle.fcirc_entries_m31x2(inp["f"], a[k], b[k])
+            bad = np.nonzero(c[k].astype(np.uint64) != exp)[0]
             assert bad.size == 0, (L, k, bad[:4])
 
 
