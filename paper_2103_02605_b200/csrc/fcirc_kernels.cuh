@@ -233,6 +233,7 @@ struct BlockArgs {
   typename F::Tw last_si;   // s_{0,0}^-1 * K   (used when k == 0)
   typename F::Tw last_k;    // K = n^-1 (x R for FieldU32)
   EmbedIO io;               // k == 0 and EMB only: embedding of the loads / truncation of the stores
+  int seq = 1;              // instance groups per CTA, one after another (sharing staged twiddles)
 };
 
 // k_block stages its twiddle slices in shared memory for the 32-bit fields (see TWS below), at
@@ -262,30 +263,25 @@ k_block(F fld, BlockArgs<F> args) {
   auto idx = [](int base_part, int slot_part) { return swz<R, T>(base_part) ^ swz<R, T>(slot_part); };
 
   const int k = args.k;
-  const int E = (int)(blockIdx.x & ((1u << k) - 1));   // sub-block index
   const int64_t batch = args.units >> k;
-  const int gbase = ((1 << k) + E) << M;   // heap-extended address base (fits: < 2n <= 2^24)
-  const int64_t inst = (int64_t)(blockIdx.x >> k) * IPC + li;
-  const bool active = inst < batch;
-  const int64_t base = ((inst << k) + E) * m;
 
-  // Twiddle staging (32-bit fields): the CTA's sub-block uses the heap slice
+  // Twiddle staging (32-bit fields): sub-block E uses the heap slice
   // {2^(k+j) + E 2^j + e' : j < M, e' < 2^j} of each table (contiguous per level).
-  // It is copied once, coalesced, into shared memory at local heap index 2^j + e' (1-based), so the
+  // It is copied, coalesced, into shared memory at local heap index 2^j + e' (1-based), so the
   // butterflies read twiddles with LDS instead of scattered L2 loads (profiles/r01c: the u32
   // k_block stalled on long_scoreboard).  Goldilocks is arithmetic-bound and keeps the LDG path;
   // so does the fused whole-product launch (k = 0), whose CTAs all share one table via L1/L2.
   Tw* twsf = reinterpret_cast<Tw*>(sm + (size_t)IPC * 2 * m);
   Tw* twsi = twsf + m;
-  if constexpr (TWS) {
+  auto stage = [&](int E) {
     for (int h = threadIdx.x + 1; h < m; h += blockDim.x) {
       const int j = 31 - __clz(h);
       const int g = (1 << (k + j)) + (E << j) + (h - (1 << j));
       twsf[tw_swz(h)] = args.twf[g];
       twsi[tw_swz(h)] = args.twi[g];
     }
-    __syncthreads();
-  }
+  };
+  int gbase = 0;   // heap-extended address base of the current sub-block (fits: < 2n <= 2^24)
   // twiddle of the pair bit `bit` at address x = tb | cs: heap entry (gbase | x) >> (bit+1), whose
   // thread part (gbase | tb) >> (bit+1) is shared by every slot of a level and whose slot part
   // cs >> (bit+1) is a compile-time offset (disjoint bits: the sum is the OR).  Staged: local heap
@@ -294,6 +290,23 @@ k_block(F fld, BlockArgs<F> args) {
     if constexpr (TWS) return staged[tw_swz(1 << (M - 1 - bit)) ^ tw_swz(tb >> (bit + 1)) ^ tw_swz(cs >> (bit + 1))];
     else return ldtw(table + ((gbase | tb) >> (bit + 1)) + (cs >> (bit + 1)));
   };
+
+  // Work assignment: CTA b -> sub-block E = b mod 2^k and seq consecutive instance groups
+  // (b >> k) seq + it, it < seq, of IPC instances each.  seq > 1 (staged launches) stages the
+  // twiddle slice once per seq sub-problems (S1 k_block -14 %).  No
+  // barrier between them: the next one's first exchange writes sa at the addresses this thread
+  // read last (exchange rule) and sb, last read in the forward levels, only after the inverse
+  // exchanges' CTA barriers.
+  const int E = (int)(blockIdx.x & ((1u << k) - 1));
+  gbase = ((1 << k) + E) << M;
+  if constexpr (TWS) {
+    stage(E);
+    __syncthreads();
+  }
+  for (int it = 0; it < args.seq; ++it) {
+  const int64_t inst = ((int64_t)(blockIdx.x >> k) * args.seq + it) * IPC + li;
+  const bool active = inst < batch;
+  const int64_t base = ((inst << k) + E) * m;
 
   T xa[R], xb[R];
   // ---- load (phase-0 addresses: slot s at s * 2^lo + t, coalesced across t)
@@ -358,6 +371,7 @@ k_block(F fld, BlockArgs<F> args) {
       }
     }
   }
+  }   // instance groups of the CTA
 }
 
 // ------------------------------------------------------------------------------------------

@@ -25,6 +25,7 @@ template <> struct FTraits<FieldU32> {
   static constexpr int MPREF = 12;  // 96 KB: two CTAs per SM
   static constexpr const char* RB = "U32_RB";
   static constexpr const char* RBF = "U32_RBF";
+  static constexpr const char* SEQ = "U32_SEQ";
   static constexpr const char* RC = "U32_RC";
   static constexpr const char* MS = "U32_MSPLIT";
   static constexpr int TMA_MIN_K = 9;   // TMA inverse column passes from this depth on; below it
@@ -35,6 +36,7 @@ template <> struct FTraits<FieldGold> {
   static constexpr int MPREF = 12;  // 64 KB: two CTAs per SM
   static constexpr const char* RB = "GOLD_RB";
   static constexpr const char* RBF = "GOLD_RBF";
+  static constexpr const char* SEQ = "GOLD_SEQ";
   static constexpr const char* RC = "GOLD_RC";
   static constexpr const char* MS = "GOLD_MSPLIT";
   static constexpr int TMA_MIN_K = 9;
@@ -44,6 +46,7 @@ template <> struct FTraits<FieldM31x2> {      // the paper's ring, 8-byte packed
   static constexpr int MPREF = 12;
   static constexpr const char* RB = "M31_RB";
   static constexpr const char* RBF = "M31_RBF";
+  static constexpr const char* SEQ = "M31_SEQ";
   static constexpr const char* RC = "M31_RC";
   static constexpr const char* MS = "M31_MSPLIT";
   static constexpr int TMA_MIN_K = 9;
@@ -81,9 +84,26 @@ static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t s
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
   if (!attr_ok) return FCIRC_ECUDA;
   const int64_t batch = args.units >> args.k;
-  const int64_t grid = ((batch + IPC - 1) / IPC) << args.k;
+  BlockArgs<F> a2 = args;
+  // staged sub-problem launches: each CTA walks seq instance groups of one sub-block, staging its
+  // twiddle slice once (FCIRC_<field>_SEQ; default: the largest power of two <= 16 that still
+  // leaves >= 1024 CTAs, about 3.5 waves of resident CTAs -- measured best for S1 (16), C3 (8)
+  // and C5 (1), profiles/r01i_sweep_seq.txt)
+  if constexpr (TWS) {
+    static const int knob_seq = knob(FTraits<F>::SEQ, 0);
+    const int64_t groups = (batch + IPC - 1) / IPC;
+    int seq = 1;
+    if (args.k > 0) {
+      if (knob_seq > 0) seq = knob_seq;
+      else
+        while (seq < 16 && ((groups / (2 * seq)) << args.k) >= 1024) seq *= 2;
+    }
+    a2.seq = (int)std::min<int64_t>(seq, groups);
+  }
+  const int64_t per_cta = (int64_t)IPC * a2.seq;
+  const int64_t grid = ((batch + per_cta - 1) / per_cta) << args.k;
   prof_begin(args.k == 0 ? 0 : 1, st);
-  kern<<<(unsigned)grid, T * IPC, smem, st>>>(fld, args);
+  kern<<<(unsigned)grid, T * IPC, smem, st>>>(fld, a2);
   prof_end(st);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
