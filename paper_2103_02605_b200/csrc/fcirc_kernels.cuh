@@ -303,8 +303,9 @@ k_block(F fld, BlockArgs<F> args) {
     stage(E);
     __syncthreads();
   }
-  for (int it = 0; it < args.seq; ++it) {
-  const int64_t inst = ((int64_t)(blockIdx.x >> k) * args.seq + it) * IPC + li;
+  const int nseq = TWS ? args.seq : 1;   // unstaged launches: one group (no loop, no extra registers)
+  for (int it = 0; it < nseq; ++it) {
+  const int64_t inst = ((int64_t)(blockIdx.x >> k) * nseq + it) * IPC + li;
   const bool active = inst < batch;
   const int64_t base = ((inst << k) + E) * m;
 

@@ -89,8 +89,8 @@ static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t s
   // twiddle slice once (FCIRC_<field>_SEQ; default: the largest power of two <= 16 that still
   // leaves >= 1024 CTAs, about 3.5 waves of resident CTAs -- measured best for S1 (16), C3 (8)
   // and C5 (1), profiles/r01i_sweep_seq.txt)
-  {
-    static const int knob_seq = knob(FTraits<F>::SEQ, TWS ? 0 : 1);
+  if constexpr (TWS) {   // (unstaged Goldilocks launches measured slower with seq > 1)
+    static const int knob_seq = knob(FTraits<F>::SEQ, 0);
     const int64_t groups = (batch + IPC - 1) / IPC;
     int seq = 1;
     if (args.k > 0) {
