@@ -148,7 +148,10 @@ static int launch_cols_fwd2(const F& fld, ColArgs<F> args, int64_t instances, cu
   constexpr int threads = W * ((1 << K) / R);
   using E = typename F::T;
   const size_t smem = (size_t)2 * (1 << K) * W * sizeof(E);
-  constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
+  // 32-bit elements fit R = 16 in 64 registers here: 1024 threads/SM (C3 forward column pass -9 %,
+  // S1 -2 %; the inverse kernel would spill, profiles/r01j_sweep_cols1024.txt)
+  constexpr int TGT = (RR <= 8 || sizeof(E) == 4) ? 1024 : 512;
+  constexpr int MINB = (threads < TGT) ? TGT / threads : 1;
   auto kern = k_cols_fwd2<F, K, R, W, MINB, EMB>;
   static const bool attr_ok =
       smem <= 48 * 1024 ||
