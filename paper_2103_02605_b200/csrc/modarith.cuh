@@ -133,16 +133,20 @@ struct FieldGold {
   // pipe): + EPS = (lo - 1) with a carry into hi unless lo == 0.  Used by the forward butterflies,
   // where it balances the pipes (+8-10 % butterflies/clk, profiles/r01e_gold_butterfly_*.jsonl);
   // the inverse butterflies keep add_c_m (faster there).
+  // (predicated updates in PTX: ptxas then emits 2 ISETP + 2 predicated adds instead of computing
+  // both alternatives and selecting with an IMAD.MOV on the FMA pipe)
   __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
-    uint32_t s0, s1, c;
-    asm("add.cc.u32  %0, %3, %5;\n\t"
-        "addc.cc.u32 %1, %4, %6;\n\t"
-        "addc.u32    %2, 0, 0;"
-        : "=r"(s0), "=r"(s1), "=r"(c) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
-    if (c) {
-      s1 = s0 == 0u ? s1 : s1 + 1u;
-      s0 = s0 - 1u;
-    }
+    uint32_t s0, s1;
+    asm("{\n\t.reg .u32 c;\n\t.reg .pred p, q;\n\t"
+        "add.cc.u32  %0, %2, %4;\n\t"
+        "addc.cc.u32 %1, %3, %5;\n\t"
+        "addc.u32    c, 0, 0;\n\t"
+        "setp.ne.u32 p, c, 0;\n\t"              // carry out of 2^64: + EPS
+        "setp.ne.and.u32 q, %0, 0, p;\n\t"      // ... which carries into hi unless lo == 0
+        "@p sub.u32  %0, %0, 1;\n\t"
+        "@q add.u32  %1, %1, 1;\n\t"
+        "}"
+        : "=&r"(s0), "=&r"(s1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
     return mk(s0, s1);
   }
   // a - b mod p for a any 64-bit value and b < p: on a borrow subtract EPS; the wrapped value is
@@ -204,11 +208,11 @@ struct FieldGold {
         : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
     return mk(r0, r1);
   }
-  // The same reduction with the final canonicalisation as selects: the 3-word chain leaves
-  // r < 2^64 with r >= p only if r_hi == 0xffffffff and r_lo != 0, and then r - p = r_lo - 1.
+  // The same reduction with the final canonicalisation as predicated updates: the 3-word chain
+  // leaves r < 2^64 with r >= p only if r_hi == 0xffffffff and r_lo != 0, and then r - p = r_lo - 1.
   __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
     uint32_t r0, r1;
-    asm("{\n\t.reg .u32 c, m, h;\n\t"
+    asm("{\n\t.reg .u32 c, m, h;\n\t.reg .pred p, q;\n\t"
         "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
         "madc.hi.cc.u32  %1, %4, 0xffffffff, %3;\n\t"
         "addc.u32        c, 0, 0;\n\t"
@@ -219,10 +223,13 @@ struct FieldGold {
         "shr.s32         h, c, 31;\n\t"
         "add.cc.u32      %0, %0, m;\n\t"
         "addc.u32        %1, %1, h;\n\t"
+        "setp.eq.u32     p, %1, 0xffffffff;\n\t"  // r >= p  <=>  r_hi == 2^32-1 and r_lo != 0
+        "setp.ne.and.u32 q, %0, 0, p;\n\t"
+        "@q sub.u32      %0, %0, 1;\n\t"          // r - p = (r_lo - 1, 0)
+        "@q mov.u32      %1, 0;\n\t"
         "}"
         : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
-    const bool big = (r1 == 0xFFFFFFFFu) & (r0 != 0u);
-    return mk(big ? r0 - 1u : r0, big ? 0u : r1);
+    return mk(r0, r1);
   }
   // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
   __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {

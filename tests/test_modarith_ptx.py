@@ -42,19 +42,11 @@ def test_add_c_m_weak_plus_canonical():
         assert r % P == (a + b) % P, (a, b, r)
 
 
-def _add_c_select(a, b):
-    """FieldGold::add_c: the asm carry chain, then the C++ select correction (+EPS on a carry)."""
-    text, nout, _ = sim.extract(SRC, "add_c")
-    s0, s1, c = sim.run(text, nout, [a & 0xFFFFFFFF, a >> 32, b & 0xFFFFFFFF, b >> 32])
-    if c:
-        s1 = s1 if s0 == 0 else (s1 + 1) & 0xFFFFFFFF
-        s0 = (s0 - 1) & 0xFFFFFFFF
-    return s0 | (s1 << 32)
-
-
-def test_add_c_select_weak_plus_canonical():
+def test_add_c_predicated_weak_plus_canonical():
+    """FieldGold::add_c: carry chain + predicated +EPS (setp / @p in the PTX)."""
+    f = sim.helper(SRC, "add_c")
     for a, b in _pairs(random.Random(11), b_max=P - 1):
-        r = _add_c_select(a, b)
+        r = f(a, b)
         assert r % P == (a + b) % P, (a, b, r)
 
 
@@ -74,19 +66,10 @@ def test_sub_w_weak_minus_weak():
         assert r % P == (a - b) % P, (a, b, r)
 
 
-def _reduce4_select(t0, t1, t2, t3):
-    """FieldGold::reduce4: the asm 3-word chain, then the C++ select canonicalisation."""
-    text, nout, _ = sim.extract(SRC, "reduce4")
-    r0, r1 = sim.run(text, nout, [t0, t1, t2, t3])
-    if r1 == 0xFFFFFFFF and r0 != 0:
-        r0, r1 = r0 - 1, 0
-    return r0 | (r1 << 32)
-
-
 @pytest.mark.parametrize("fn", ["reduce4_m", "reduce4"])
 @pytest.mark.parametrize("seed", [4, 5])
 def test_reduce4_canonical(seed, fn):
-    f = sim.helper(SRC, "reduce4_m") if fn == "reduce4_m" else _reduce4_select
+    f = sim.helper(SRC, fn)
     rng = random.Random(seed)
     words = [0, 1, 0xFFFFFFFF, 0xFFFFFFFE, 0x80000000]
     cases = [(a, b, c, d) for a in words for b in words for c in words for d in words]

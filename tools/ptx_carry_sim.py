@@ -10,6 +10,7 @@ becomes `IMAD.X m, RZ, RZ, -1, P` = carry - 1):
                                 sub.cc:  d = a + ~b + 1,   CF = carry out (= NOT borrow)
                                 subc:    d = a + ~b + CF
                                 mad.lo.cc / madc.hi.cc: lo/hi 32 bits of a*b, plus c (+ CF)
+    setp.{eq,ne}[.and].u32 and @p / @!p predication: plain predicate semantics
 
 so a helper can be checked exhaustively on edge values and randomly against Python integers
 without a GPU.  Used by tests/test_modarith_ptx.py.
@@ -27,6 +28,10 @@ def extract(src: str, fn: str):
     j = src.index("asm(", i)
     k = src.index(");", j)
     block = src[j + 4:k]
+    # drop C++ comments between the string literals (they may contain ':'): whole comment lines
+    # and comments after a literal's closing quote
+    block = "\n".join(l for l in block.split("\n") if not l.strip().startswith("//"))
+    block = re.sub(r'("\s*)//[^\n]*', r"\1", block)
     parts = block.split(":")
     text = "".join(re.findall(r'"((?:[^"\\]|\\.)*)"', parts[0]))
     text = text.replace("\\n", "\n").replace("\\t", " ")
@@ -42,6 +47,7 @@ def run(text: str, nout: int, inputs):
     for i in range(nout):
         regs[f"%{i}"] = 0
     cf = 0
+    preds = {}
 
     def val(tok):
         tok = tok.strip()
@@ -55,8 +61,22 @@ def run(text: str, nout: int, inputs):
             continue
         line = line.split("//")[0].strip().rstrip(";")
         op, rest = line.split(None, 1)
+        if op.startswith("@"):           # predicated instruction: @p op ... / @!p op ...
+            neg = op.startswith("@!")
+            pv = preds[op[2:] if neg else op[1:]]
+            if pv == neg:
+                continue
+            op, rest = rest.split(None, 1)
         args = [a.strip() for a in rest.split(",")]
         d = args[0]
+        if op.startswith("setp."):       # setp.{eq,ne}[.and].u32 p, a, b[, q]
+            parts = op.split(".")
+            cmp = parts[1]
+            v = (val(args[1]) == val(args[2])) if cmp == "eq" else (val(args[1]) != val(args[2]))
+            if "and" in parts:
+                v = v and preds[args[3]]
+            preds[d] = v
+            continue
         if op in ("add.cc.u32", "addc.cc.u32", "addc.u32", "add.u32"):
             cin = cf if op.startswith("addc") else 0
             r = val(args[1]) + val(args[2]) + cin
