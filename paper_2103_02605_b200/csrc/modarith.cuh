@@ -102,39 +102,23 @@ struct FieldGold {
   static constexpr uint64_t P = 0xFFFFFFFF00000001ull;
   static constexpr uint64_t EPS = 0xFFFFFFFFull;  // 2^64 mod p
 
-  // All helpers work on 32-bit halves with explicit PTX carry chains.  A wrap-around correction
-  // (+-EPS when a 64-bit add/sub carried/borrowed) is applied arithmetically, never by setp /
-  // selp / predication: after a subtract chain `subc.u32 m, 0, 0` yields m = -borrow (0 or
-  // 0xffffffff = EPS's low word) and the correction is one more subtract chain; after an add
-  // chain `addc.u32 m, 0, 0` yields the carry and `mad.lo.cc m * EPS` adds the correction.  (PTX
-  // carry flags are the hardware carry: after an add, `subc m, 0, 0` gives carry - 1, NOT -carry,
-  // so add and subtract chains are never mixed.)  ptxas maps the materialisations to IMAD.X /
-  // IMAD on the FMA pipe, which offloads the saturated ALU pipe
-  // (profiles/r01c_ncu_full_k_block.txt: the predicated form spent ~11 SEL/ISETP/PLOP3 per modmul).
+  // All helpers work on 32-bit halves with explicit PTX carry chains.  The wrap-around corrections
+  // (+-EPS when a 64-bit add/sub carried/borrowed, and the final r >= p test of a reduction) are
+  // written the way that measured fewest SASS instructions: after an add chain, the carry becomes
+  // a predicate and the correction two predicated adds (add_c, reduce4: ptxas emits ISETP + @P
+  // VIADD instead of computing both alternatives and selecting with an IMAD.MOV, -8 % instructions
+  // per butterfly, profiles/r01k_sweep_gold_predicated_ab.txt); after a subtract chain
+  // `subc.u32 m, 0, 0` yields m = -borrow (0 or 0xffffffff = EPS's low word) and the correction is
+  // one more subtract chain (sub_c, sub_w).  (PTX carry flags are the hardware carry: after an add,
+  // `subc m, 0, 0` gives carry - 1, NOT -carry, so add and subtract chains are never mixed;
+  // tests/test_modarith_ptx.py executes every chain under that model.)
   __device__ __forceinline__ static uint32_t lo32(uint64_t x) { return (uint32_t)x; }
   __device__ __forceinline__ static uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
   __device__ __forceinline__ static uint64_t mk(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
 
-  // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS;
-  // a + b - 2^64 + EPS <= (2^64-1) + (p-1) - 2^64 + EPS = 2^64 - 2: no second carry.  Weak result.
-  __device__ __forceinline__ static uint64_t add_c_m(uint64_t a, uint64_t b) {
-    uint32_t s0, s1;
-    asm("{\n\t.reg .u32 m;\n\t"
-        "add.cc.u32  %0, %2, %4;\n\t"
-        "addc.cc.u32 %1, %3, %5;\n\t"
-        "addc.u32    m, 0, 0;\n\t"                 // m = carry (0/1)
-        "mad.lo.cc.u32 %0, m, 0xffffffff, %0;\n\t" // + EPS * carry
-        "addc.u32    %1, %1, 0;\n\t"
-        "}"
-        : "=&r"(s0), "=&r"(s1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
-    return mk(s0, s1);
-  }
-  // The same sum with the correction as selects (ALU pipe) instead of a mask multiply-add (FMA
-  // pipe): + EPS = (lo - 1) with a carry into hi unless lo == 0.  Used by the forward butterflies,
-  // where it balances the pipes (+8-10 % butterflies/clk, profiles/r01e_gold_butterfly_*.jsonl);
-  // the inverse butterflies keep add_c_m (faster there).
-  // (predicated updates in PTX: ptxas then emits 2 ISETP + 2 predicated adds instead of computing
-  // both alternatives and selecting with an IMAD.MOV on the FMA pipe)
+  // a + b mod p for a any 64-bit value and b < p (canonical): on a carry out of 2^64 add EPS
+  // (= lo - 1, with a carry into hi unless lo == 0); a + b - 2^64 + EPS <= 2^64 - 2: no second
+  // carry.  Weak result.
   __device__ __forceinline__ static uint64_t add_c(uint64_t a, uint64_t b) {
     uint32_t s0, s1;
     asm("{\n\t.reg .u32 c;\n\t.reg .pred p, q;\n\t"
@@ -185,31 +169,7 @@ struct FieldGold {
   //       (V in (-2^32, 2^65 - 2^33]);
   //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
   //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
-  //   canonicalise: u = r + EPS carries iff r >= p; then r += EPS * carry (mod 2^64) = r - p.
-  __device__ __forceinline__ static uint64_t reduce4_m(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
-    uint32_t r0, r1;
-    asm("{\n\t.reg .u32 c, m, h;\n\t"
-        "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
-        "madc.hi.cc.u32  %1, %4, 0xffffffff, %3;\n\t"
-        "addc.u32        c, 0, 0;\n\t"
-        "sub.cc.u32      %0, %0, %5;\n\t"
-        "subc.cc.u32     %1, %1, 0;\n\t"
-        "subc.u32        c, c, 0;\n\t"
-        "neg.s32         m, c;\n\t"
-        "shr.s32         h, c, 31;\n\t"
-        "add.cc.u32      %0, %0, m;\n\t"
-        "addc.u32        %1, %1, h;\n\t"
-        "add.cc.u32      m, %0, 0xffffffff;\n\t"   // carry out iff r >= p
-        "addc.cc.u32     h, %1, 0;\n\t"
-        "addc.u32        m, 0, 0;\n\t"
-        "mad.lo.cc.u32   %0, m, 0xffffffff, %0;\n\t"  // r + EPS * carry (mod 2^64) = r - p
-        "addc.u32        %1, %1, 0;\n\t"
-        "}"
-        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
-    return mk(r0, r1);
-  }
-  // The same reduction with the final canonicalisation as predicated updates: the 3-word chain
-  // leaves r < 2^64 with r >= p only if r_hi == 0xffffffff and r_lo != 0, and then r - p = r_lo - 1.
+  //   canonicalise: r >= p only if r_hi == 0xffffffff and r_lo != 0, and then r - p = (r_lo - 1, 0).
   __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
     uint32_t r0, r1;
     asm("{\n\t.reg .u32 c, m, h;\n\t.reg .pred p, q;\n\t"
@@ -237,10 +197,6 @@ struct FieldGold {
     const uint64_t lo = a * b, hi = __umul64hi(a, b);
     return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
   }
-  __device__ __forceinline__ static uint64_t mul_m(uint64_t a, uint64_t b) {
-    const uint64_t lo = a * b, hi = __umul64hi(a, b);
-    return reduce4_m(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
-  }
   __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
 
   // forward a: inputs weak; t = s y canonical -> single corrections
@@ -258,9 +214,7 @@ struct FieldGold {
     y = sub_w(t, Y);
   }
   // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical.
-  // Select forms: in the isolated-butterfly microbenchmark the mask forms were faster for this
-  // butterfly, but inside k_block (mixed with the forward butterflies, FMA-heavy pipe at 80 %)
-  // the select forms measured 1.6 % faster (profiles/r01f_sweep_gold_inv_select.txt).
+  // (add_c and mul use the predicated corrections, like the forward butterflies.)
   __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
     const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
     const uint64_t d = sub_c(u, v);   // canonical
@@ -268,10 +222,10 @@ struct FieldGold {
     v = d;
   }
   __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
-    const uint64_t s = add_c_m(u, v);
+    const uint64_t s = add_c(u, v);
     const uint64_t d = sub_c(u, v);
-    u = mul_m(s, si_k);
-    v = mul_m(d, k);
+    u = mul(s, si_k);
+    v = mul(d, k);
   }
   __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
   __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {

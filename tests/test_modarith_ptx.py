@@ -35,13 +35,6 @@ def _pairs(rng, n=3000, a_max=M64, b_max=M64):
         yield rng.randint(max(0, a_max - (1 << 34)), a_max), rng.randint(max(0, b_max - (1 << 34)), b_max)
 
 
-def test_add_c_m_weak_plus_canonical():
-    f = sim.helper(SRC, "add_c_m")
-    for a, b in _pairs(random.Random(1), b_max=P - 1):
-        r = f(a, b)
-        assert r % P == (a + b) % P, (a, b, r)
-
-
 def test_add_c_predicated_weak_plus_canonical():
     """FieldGold::add_c: carry chain + predicated +EPS (setp / @p in the PTX)."""
     f = sim.helper(SRC, "add_c")
@@ -66,7 +59,7 @@ def test_sub_w_weak_minus_weak():
         assert r % P == (a - b) % P, (a, b, r)
 
 
-@pytest.mark.parametrize("fn", ["reduce4_m", "reduce4"])
+@pytest.mark.parametrize("fn", ["reduce4"])
 @pytest.mark.parametrize("seed", [4, 5])
 def test_reduce4_canonical(seed, fn):
     f = sim.helper(SRC, fn)

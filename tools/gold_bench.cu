@@ -1066,7 +1066,7 @@ static int run(const char* tag, int nsm) {
 int main() {
   int nsm; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
   int rc = run<FieldGoldSel>("r01b predicated corrections (FieldGoldSel)", nsm);
-  rc |= run<FieldGold>("mask corrections (FieldGold, current)", nsm);
+  rc |= run<FieldGold>("predicated corrections (FieldGold, current)", nsm);
   rc |= run<FieldGoldW>("mad.wide corrections (FieldGoldW)", nsm);
   rc |= run<FieldGoldW2>("W + FMA borrow corrections + opaque zero (FieldGoldW2)", nsm);
   rc |= run<FieldGoldG3>("select-based canonicalisation (FieldGoldG3)", nsm);
