@@ -284,8 +284,8 @@ static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t s
 
 // Column-pass selection (measured, profiles/r01e_sweep_cols2.txt):
 //   forward, plain, K >= 6      -> k_cols_fwd2 (a and b per thread)        FCIRC_COLS2=0 disables
-//   forward, polynomial / any-n -> k_cols_fwd2<EMB>
-//   forward, limb embed         -> k_cols<EMB> (the per-limb loads favour one operand per thread)
+//   forward, embedded operands  -> k_cols_fwd2<EMB> (polynomial, any-n, and limbs: C5's forward
+//                                  column pass 0.118 -> 0.090 ms at 1024 threads/SM, r01l sweep)
 //   inverse, K >= TMA_MIN_K     -> k_cols_tma (persistent, TMA double-buffered)  FCIRC_TMA=0 disables
 //   inverse, 6 <= K < TMA_MIN_K -> k_cols_inv2 (two column groups per thread)   FCIRC_INV2=0 disables
 //   otherwise                   -> k_cols (R = 16, or the FCIRC_<field>_RC variant)
@@ -297,7 +297,7 @@ static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cud
   using E = typename F::T;
   const int mode = args.io.mode;
   if constexpr (!INV && K >= 4 && K <= 10) {
-    if (use_fwd2 && (mode == EMB_POLY || mode == EMB_ANYN)) return launch_cols_fwd2<F, K, 16, true>(fld, args, inst, st);
+    if (use_fwd2 && mode != EMB_PLAIN) return launch_cols_fwd2<F, K, 16, true>(fld, args, inst, st);
     if (use_fwd2 && mode == EMB_PLAIN && K >= 6) {
       if (r == 8) return launch_cols_fwd2<F, K, 8>(fld, args, inst, st);
       return launch_cols_fwd2<F, K, 16>(fld, args, inst, st);
