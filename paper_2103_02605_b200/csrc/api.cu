@@ -407,7 +407,7 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   k_crt_digits<<<(unsigned)(batch * nseg), kCarryThreads, 0, st>>>(r1, r2, r3, L, ncoef, nd, nseg, g, E, S);
   prof_end(st);
   prof_begin(4, st);
-  k_carry_top<<<(unsigned)batch, 32, 0, st>>>(S, nseg, batch);
+  k_carry_top<<<(unsigned)batch, kTopThreads, 0, st>>>(S, nseg);
   prof_end(st);
   prof_begin(4, st);
   k_carry_apply<<<(unsigned)(batch * nseg), kCarryThreads, 0, st>>>(E, nd, nseg, S, z, nx + ny);

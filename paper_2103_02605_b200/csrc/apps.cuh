@@ -63,9 +63,11 @@ constexpr int kCarrySeg = kCarryThreads * kCarryPer;   // 2048 digits = 1024 out
 struct GP { uint32_t g, p; };
 __device__ __forceinline__ GP gp_compose(GP x, GP y) { return {y.g | (y.p & x.g), y.p & x.p}; }  // x then y
 
-// block-wide exclusive scan of (G, P) (identity (0, 1)); returns this thread's prefix, *total
+// block-wide exclusive scan of (G, P) over NT threads (identity (0, 1)); returns this thread's
+// prefix, *total
+template <int NT = kCarryThreads>
 __device__ __forceinline__ GP gp_block_exscan(GP v, GP* total) {
-  __shared__ uint32_t wg[kCarryThreads / 32], wp[kCarryThreads / 32];
+  __shared__ uint32_t wg[NT / 32], wp[NT / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   GP inc = v;
 #pragma unroll
@@ -78,7 +80,7 @@ __device__ __forceinline__ GP gp_block_exscan(GP v, GP* total) {
   GP wpre{0u, 1u};
   for (int w = 0; w < warp; ++w) wpre = gp_compose(wpre, GP{wg[w], wp[w]});
   GP tot{0u, 1u};
-  for (int w = 0; w < kCarryThreads / 32; ++w) tot = gp_compose(tot, GP{wg[w], wp[w]});
+  for (int w = 0; w < NT / 32; ++w) tot = gp_compose(tot, GP{wg[w], wp[w]});
   *total = tot;
   GP ex{__shfl_up_sync(0xffffffffu, inc.g, 1), __shfl_up_sync(0xffffffffu, inc.p, 1)};
   if (lane == 0) ex = GP{0u, 1u};
@@ -142,29 +144,23 @@ k_crt_digits(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2, c
   if (threadIdx.x == 0) seg_gp[blockIdx.x] = tot.g | (tot.p << 1);
 }
 
-// one warp per integer: carry into every segment (exclusive scan of the segment pairs)
-__global__ void k_carry_top(uint32_t* __restrict__ seg_gp, int64_t nseg, int64_t batch) {
-  const int64_t inst = blockIdx.x;
-  if (inst >= batch) return;
-  uint32_t* s = seg_gp + inst * nseg;
-  const int lane = threadIdx.x;
-  uint32_t carry = 0;   // carry into the current 32-segment window
-  for (int64_t w0 = 0; w0 < nseg; w0 += 32) {
-    const int64_t i = w0 + lane;
-    const uint32_t v = i < nseg ? s[i] : 2u;   // identity (g = 0, p = 1)
-    GP inc{v & 1u, v >> 1};
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      GP o{__shfl_up_sync(0xffffffffu, inc.g, off), __shfl_up_sync(0xffffffffu, inc.p, off)};
-      if (lane >= off) inc = gp_compose(o, inc);
-    }
-    GP ex{__shfl_up_sync(0xffffffffu, inc.g, 1), __shfl_up_sync(0xffffffffu, inc.p, 1)};
-    if (lane == 0) ex = GP{0u, 1u};
-    const uint32_t cin = ex.g | (ex.p & carry);
-    const uint32_t last_g = __shfl_sync(0xffffffffu, inc.g, 31), last_p = __shfl_sync(0xffffffffu, inc.p, 31);
-    __syncwarp();
-    if (i < nseg) s[i] = cin;   // overwrite with the carry into segment i
-    carry = last_g | (last_p & carry);
+// one CTA of kTopThreads per integer: carry into every segment (exclusive scan of the segment
+// pairs).  Each thread owns a contiguous run of segments, so all loads are independent (the former
+// one-warp loop serialised a global-load round trip per 32 segments).
+constexpr int kTopThreads = 1024;
+__global__ void __launch_bounds__(kTopThreads) k_carry_top(uint32_t* __restrict__ seg_gp, int64_t nseg) {
+  uint32_t* s = seg_gp + (int64_t)blockIdx.x * nseg;
+  const int64_t per = (nseg + kTopThreads - 1) / kTopThreads;
+  const int64_t b0 = (int64_t)threadIdx.x * per, b1 = b0 + per < nseg ? b0 + per : nseg;
+  GP agg{0u, 1u};
+  for (int64_t i = b0; i < b1; ++i) agg = gp_compose(agg, GP{s[i] & 1u, s[i] >> 1});
+  GP tot;
+  GP c = gp_block_exscan<kTopThreads>(agg, &tot);   // carry-in state of segment b0 (g = carry)
+  __syncthreads();                                   // every thread has read its run
+  for (int64_t i = b0; i < b1; ++i) {
+    const GP v{s[i] & 1u, s[i] >> 1};   // re-read (own run only: no other thread writes it)
+    s[i] = c.g;                         // carry into segment i
+    c = gp_compose(c, v);
   }
 }
 
