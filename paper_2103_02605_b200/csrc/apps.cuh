@@ -99,46 +99,50 @@ __device__ __forceinline__ GP local_gp(const uint32_t e[kCarryPer]) {
   return acc;
 }
 
-// One CTA per (integer, segment of kCarrySeg digits): Garner CRT of the coefficients the segment
-// needs (its own and 6 below it) into shared memory, the digits
+// One CTA per (integer, segment of kCarrySeg digits); thread t owns the kCarryPer digits
+// j0 .. j0 + kCarryPer - 1, j0 = segment start + t kCarryPer.  The digit sums
 //   D_j = sum_{i<6} chunk16_i(V_{j-i}) (< 6 * 2^16),  E_j = (D_j mod 2^16) + floor(D_{j-1} / 2^16)
-// (< 2^16 + 6, so every carry is 0 or 1), written to E for the final pass, and the segment's
-// carry-lookahead pair (G, P) -- one launch instead of CRT, digit and segment kernels, and no
-// 128-bit coefficient array in global memory.
+// (< 2^16 + 6, so every carry is 0 or 1) need the CRT values V_k for k in [j0 - 6, j0 + 8): the
+// thread computes those 14 Garner reconstructions itself (the 6 below its own digits are also
+// computed by its neighbour) and keeps them in registers -- no shared-memory chunk table (the
+// former one ran into MIO throttling: 16.5 stall cycles per issue, profiles/r01l_ncu_c5.txt).  It
+// writes E for the final pass and the segment's carry-lookahead pair (G, P).
 constexpr int kHalo = 6;
 __global__ void __launch_bounds__(kCarryThreads)
 k_crt_digits(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2, const uint32_t* __restrict__ r3,
              int64_t L, int64_t ncoef, int64_t nd, int64_t nseg, GarnerConsts g, uint32_t* __restrict__ E,
              uint32_t* __restrict__ seg_gp) {
-  __shared__ uint16_t ch[kCarrySeg + kHalo][6];   // 16-bit chunks of V_k, k = j0 - kHalo + row
+  constexpr int NV = kCarryPer + kHalo;   // V_{j0 - kHalo + q}, q < NV
   const int64_t inst = blockIdx.x / nseg, sg = blockIdx.x - inst * nseg;
-  const int64_t j0 = sg * kCarrySeg;
+  const int64_t j0 = sg * kCarrySeg + (int64_t)threadIdx.x * kCarryPer;
   const uint32_t *a1 = r1 + inst * L, *a2 = r2 + inst * L, *a3 = r3 + inst * L;
-  for (int q = threadIdx.x; q < kCarrySeg + kHalo; q += kCarryThreads) {
+  uint32_t w[NV][3];   // 96-bit V as three 32-bit words (V < p1 p2 p3 < 2^90)
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
     const int64_t k = j0 - kHalo + q;
     uint64_t lo = 0, hi = 0;
-    if (k >= 0 && k < ncoef) garner(a1[k], a2[k], a3[k], g, lo, hi);
-#pragma unroll
-    for (int i = 0; i < 6; ++i) ch[q][i] = (uint16_t)((i < 4 ? lo >> (16 * i) : hi >> (16 * (i - 4))) & 0xFFFFu);
+    if (k >= 0 && k < ncoef) garner(__ldg(a1 + k), __ldg(a2 + k), __ldg(a3 + k), g, lo, hi);
+    w[q][0] = (uint32_t)lo;
+    w[q][1] = (uint32_t)(lo >> 32);
+    w[q][2] = (uint32_t)hi;
   }
-  __syncthreads();
+  // 16-bit chunk i of V at row q
+  auto chunk = [&](int q, int i) -> uint32_t { return (w[q][i >> 1] >> (16 * (i & 1))) & 0xFFFFu; };
   uint32_t e[kCarryPer];
-  const int jl0 = threadIdx.x * kCarryPer;   // local digit index
 #pragma unroll
-  for (int d = 0; d < kCarryPer; ++d) {
-    const int jl = jl0 + d;                  // digit j = j0 + jl uses rows jl + kHalo - i
+  for (int d = 0; d < kCarryPer; ++d) {   // digit j = j0 + d uses rows d + kHalo - i
     uint32_t D = 0, Dm = 0;
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
-      D += ch[jl + kHalo - i][i];
-      Dm += ch[jl + kHalo - 1 - i][i];
+      D += chunk(d + kHalo - i, i);
+      Dm += chunk(d + kHalo - 1 - i, i);
     }
-    e[d] = (j0 + jl < nd) ? (D & 0xFFFFu) + (Dm >> 16) : 0u;
+    e[d] = (j0 + d < nd) ? (D & 0xFFFFu) + (Dm >> 16) : 0u;
   }
   uint32_t* Ei = E + inst * nd;
 #pragma unroll
   for (int d = 0; d < kCarryPer; ++d)
-    if (j0 + jl0 + d < nd) Ei[j0 + jl0 + d] = e[d];
+    if (j0 + d < nd) Ei[j0 + d] = e[d];
   GP tot;
   gp_block_exscan(local_gp(e), &tot);
   if (threadIdx.x == 0) seg_gp[blockIdx.x] = tot.g | (tot.p << 1);
