@@ -103,10 +103,10 @@ __device__ __forceinline__ GP local_gp(const uint32_t e[kCarryPer]) {
 // j0 .. j0 + kCarryPer - 1, j0 = segment start + t kCarryPer.  The digit sums
 //   D_j = sum_{i<6} chunk16_i(V_{j-i}) (< 6 * 2^16),  E_j = (D_j mod 2^16) + floor(D_{j-1} / 2^16)
 // (< 2^16 + 6, so every carry is 0 or 1) need the CRT values V_k for k in [j0 - 6, j0 + 8): the
-// thread computes those 14 Garner reconstructions itself (the 6 below its own digits are also
-// computed by its neighbour) and keeps them in registers -- no shared-memory chunk table (the
-// former one ran into MIO throttling: 16.5 stall cycles per issue, profiles/r01l_ncu_c5.txt).  It
-// writes E for the final pass and the segment's carry-lookahead pair (G, P).
+// thread computes its own 8 Garner reconstructions and takes the 6 below from its neighbour, all
+// in registers -- no shared-memory chunk table (the former one ran into MIO throttling: 16.5
+// stall cycles per issue, profiles/r01l_ncu_c5.txt).  It writes E for the final pass and the
+// segment's carry-lookahead pair (G, P).
 constexpr int kHalo = 6;
 __global__ void __launch_bounds__(kCarryThreads)
 k_crt_digits(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2, const uint32_t* __restrict__ r3,
@@ -117,14 +117,40 @@ k_crt_digits(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2, c
   const int64_t j0 = sg * kCarrySeg + (int64_t)threadIdx.x * kCarryPer;
   const uint32_t *a1 = r1 + inst * L, *a2 = r2 + inst * L, *a3 = r3 + inst * L;
   uint32_t w[NV][3];   // 96-bit V as three 32-bit words (V < p1 p2 p3 < 2^90)
-#pragma unroll
-  for (int q = 0; q < NV; ++q) {
+  auto crt = [&](int q) {
     const int64_t k = j0 - kHalo + q;
     uint64_t lo = 0, hi = 0;
     if (k >= 0 && k < ncoef) garner(__ldg(a1 + k), __ldg(a2 + k), __ldg(a3 + k), g, lo, hi);
     w[q][0] = (uint32_t)lo;
     w[q][1] = (uint32_t)(lo >> 32);
     w[q][2] = (uint32_t)hi;
+  };
+#pragma unroll
+  for (int q = kHalo; q < NV; ++q) crt(q);   // this thread's own coefficients
+  // the halo rows 0..5 are the previous thread's last six: a warp shuffle, through shared memory
+  // across warp boundaries, recomputed only by thread 0 (the previous segment's coefficients)
+  __shared__ uint32_t edge[kCarryThreads / 32][kHalo][3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 31)
+#pragma unroll
+    for (int r = 0; r < kHalo; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) edge[warp][r][c] = w[kCarryPer + r][c];
+#pragma unroll
+  for (int r = 0; r < kHalo; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) w[r][c] = __shfl_up_sync(0xffffffffu, w[kCarryPer + r][c], 1);
+  __syncthreads();
+  if (lane == 0) {
+    if (warp > 0) {
+#pragma unroll
+      for (int r = 0; r < kHalo; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) w[r][c] = edge[warp - 1][r][c];
+    } else {
+#pragma unroll
+      for (int q = 0; q < kHalo; ++q) crt(q);
+    }
   }
   // 16-bit chunk i of V at row q
   auto chunk = [&](int q, int i) -> uint32_t { return (w[q][i >> 1] >> (16 * (i & 1))) & 0xFFFFu; };
