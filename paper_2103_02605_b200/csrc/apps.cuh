@@ -125,8 +125,38 @@ k_crt_digits(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2, c
     w[q][1] = (uint32_t)(lo >> 32);
     w[q][2] = (uint32_t)hi;
   };
+  {   // this thread's own coefficients: 8 consecutive words per prime as two 16-byte loads when
+      // they lie inside the instance's L-word residue arrays (j0 is a multiple of 8; the arrays are
+      // 16-byte aligned for L % 4 == 0), else guarded scalar loads
+    uint32_t v1[kCarryPer], v2[kCarryPer], v3[kCarryPer];
+    if ((L & 3) != 0 || j0 + kCarryPer > L) {
 #pragma unroll
-  for (int q = kHalo; q < NV; ++q) crt(q);   // this thread's own coefficients
+      for (int d = 0; d < kCarryPer; ++d) {
+        const bool in = j0 + d < ncoef;
+        v1[d] = in ? __ldg(a1 + j0 + d) : 0u;
+        v2[d] = in ? __ldg(a2 + j0 + d) : 0u;
+        v3[d] = in ? __ldg(a3 + j0 + d) : 0u;
+      }
+    } else {
+#pragma unroll
+    for (int h = 0; h < kCarryPer; h += 4) {
+      const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(a1 + j0 + h));
+      const uint4 x2 = __ldg(reinterpret_cast<const uint4*>(a2 + j0 + h));
+      const uint4 x3 = __ldg(reinterpret_cast<const uint4*>(a3 + j0 + h));
+      v1[h] = x1.x; v1[h + 1] = x1.y; v1[h + 2] = x1.z; v1[h + 3] = x1.w;
+      v2[h] = x2.x; v2[h + 1] = x2.y; v2[h + 2] = x2.z; v2[h + 3] = x2.w;
+      v3[h] = x3.x; v3[h + 1] = x3.y; v3[h + 2] = x3.z; v3[h + 3] = x3.w;
+    }
+    }
+#pragma unroll
+    for (int d = 0; d < kCarryPer; ++d) {
+      uint64_t lo = 0, hi = 0;
+      if (j0 + d < ncoef) garner(v1[d], v2[d], v3[d], g, lo, hi);
+      w[kHalo + d][0] = (uint32_t)lo;
+      w[kHalo + d][1] = (uint32_t)(lo >> 32);
+      w[kHalo + d][2] = (uint32_t)hi;
+    }
+  }
   // the halo rows 0..5 are the previous thread's last six: a warp shuffle, through shared memory
   // across warp boundaries, recomputed only by thread 0 (the previous segment's coefficients)
   __shared__ uint32_t edge[kCarryThreads / 32][kHalo][3];
