@@ -88,6 +88,11 @@ __device__ __forceinline__ GP gp_block_exscan(GP v, GP* total) {
 }
 
 __device__ __forceinline__ void load_digits(const uint32_t* Ei, int64_t nd, int64_t j0, uint32_t e[kCarryPer]) {
+  if ((nd & 3) == 0 && j0 + kCarryPer <= nd) {   // 16-byte loads (E rows are 16-byte aligned)
+    const uint4 x = reinterpret_cast<const uint4*>(Ei + j0)[0], y = reinterpret_cast<const uint4*>(Ei + j0)[1];
+    e[0] = x.x; e[1] = x.y; e[2] = x.z; e[3] = x.w; e[4] = y.x; e[5] = y.y; e[6] = y.z; e[7] = y.w;
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < kCarryPer; ++q) e[q] = (j0 + q < nd) ? Ei[j0 + q] : 0u;
 }
@@ -196,9 +201,14 @@ k_crt_digits(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2, c
     e[d] = (j0 + d < nd) ? (D & 0xFFFFu) + (Dm >> 16) : 0u;
   }
   uint32_t* Ei = E + inst * nd;
+  if ((nd & 3) == 0 && j0 + kCarryPer <= nd) {   // 16-byte stores (E is our aligned workspace)
+    reinterpret_cast<uint4*>(Ei + j0)[0] = make_uint4(e[0], e[1], e[2], e[3]);
+    reinterpret_cast<uint4*>(Ei + j0)[1] = make_uint4(e[4], e[5], e[6], e[7]);
+  } else {
 #pragma unroll
-  for (int d = 0; d < kCarryPer; ++d)
-    if (j0 + d < nd) Ei[j0 + d] = e[d];
+    for (int d = 0; d < kCarryPer; ++d)
+      if (j0 + d < nd) Ei[j0 + d] = e[d];
+  }
   GP tot;
   gp_block_exscan(local_gp(e), &tot);
   if (threadIdx.x == 0) seg_gp[blockIdx.x] = tot.g | (tot.p << 1);
@@ -235,14 +245,22 @@ k_carry_apply(const uint32_t* __restrict__ E, int64_t nd, int64_t nseg, const ui
   const GP pre = gp_block_exscan(local_gp(e), &tot);
   uint32_t c = pre.g | (pre.p & seg_cin[blockIdx.x]);   // carry into this thread's first digit
   uint32_t* zi = z + inst * nw;
+  uint32_t out[kCarryPer / 2];
 #pragma unroll
   for (int q = 0; q < kCarryPer; q += 2) {
     const uint32_t s0 = (e[q] & 0xFFFFu) + c;
     c = (e[q] >> 16) | (s0 >> 16);
     const uint32_t s1 = (e[q + 1] & 0xFFFFu) + c;
     c = (e[q + 1] >> 16) | (s1 >> 16);
-    const int64_t w = (j0 + q) >> 1;
-    if (w < nw) zi[w] = (s0 & 0xFFFFu) | ((s1 & 0xFFFFu) << 16);
+    out[q >> 1] = (s0 & 0xFFFFu) | ((s1 & 0xFFFFu) << 16);
+  }
+  const int64_t w0 = j0 >> 1;   // kCarryPer / 2 = 4 output words
+  if (w0 + 4 <= nw && (reinterpret_cast<uintptr_t>(zi + w0) & 15u) == 0) {
+    *reinterpret_cast<uint4*>(zi + w0) = make_uint4(out[0], out[1], out[2], out[3]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kCarryPer / 2; ++q)
+      if (w0 + q < nw) zi[w0 + q] = out[q];
   }
 }
 
