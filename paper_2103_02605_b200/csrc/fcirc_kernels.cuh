@@ -555,7 +555,7 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
 // k_cols_inv2: the inverse column pass with two column groups (c and c + W) per thread, sharing
 // every twiddle load and doubling the independent butterflies per level (plain operands).
 // ------------------------------------------------------------------------------------------
-template <class F, int K, int R, int W, int MINB = 1>
+template <class F, int K, int R, int W, int MINB = 1, bool EMB = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols_inv2(F fld, ColArgs<F> args) {
   using T = typename F::T;
@@ -590,11 +590,21 @@ k_cols_inv2(F fld, ColArgs<F> args) {
       fld.inv(xb[s0], xb[s1], tw);
     }
   });
+  if constexpr (EMB) {   // truncating stores of the polynomial / any-n applications
+    const int64_t col = base - inst * args.n;
 #pragma unroll
-  for (int s = 0; s < R; ++s) {
-    const int64_t ad = base + (int64_t)(PH::ins_t(0, t) + PH::cslot(0, s)) * m;
-    args.dst0[ad] = xa[s];
-    args.dst0[ad + W] = xb[s];
+    for (int s = 0; s < R; ++s) {
+      const int64_t pos = col + (int64_t)(PH::ins_t(0, t) + PH::cslot(0, s)) * m;
+      io_store(args.dst0, inst, pos, args.n, xa[s], args.io);
+      io_store(args.dst0, inst, pos + W, args.n, xb[s], args.io);
+    }
+  } else {
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int64_t ad = base + (int64_t)(PH::ins_t(0, t) + PH::cslot(0, s)) * m;
+      args.dst0[ad] = xa[s];
+      args.dst0[ad + W] = xb[s];
+    }
   }
 }
 

@@ -167,14 +167,14 @@ static int launch_cols_fwd2(const F& fld, ColArgs<F> args, int64_t instances, cu
 }
 
 // inverse column pass, two column groups per thread (plain operands; needs m >= 2 W)
-template <class F, int K, int RR>
+template <class F, int K, int RR, bool EMB = false>
 static int launch_cols_inv2(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
   constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
   constexpr int threads = W * ((1 << K) / R);
   using E = typename F::T;
   const size_t smem = (size_t)2 * (1 << K) * W * sizeof(E);
   constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
-  auto kern = k_cols_inv2<F, K, R, W, MINB>;
+  auto kern = k_cols_inv2<F, K, R, W, MINB, EMB>;
   static const bool attr_ok =
       smem <= 48 * 1024 ||
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
@@ -303,8 +303,13 @@ static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cud
       return launch_cols_fwd2<F, K, 16>(fld, args, inst, st);
     }
   }
-  if (mode != EMB_PLAIN) {  // application embeddings: one variant (R = 16)
-    if (INV && !emb_truncates(mode)) return launch_cols<F, K, INV, 16>(fld, args, inst, st);
+  // application embeddings: the forward pass reads embedded operands (above); the inverse pass of
+  // a truncating embedding (polynomial, any-n) stores through EMB; a limb embedding's inverse
+  // output is a plain [batch][n] array and takes the plain selection below
+  if (!INV && mode != EMB_PLAIN) return launch_cols<F, K, INV, 16, true>(fld, args, inst, st);
+  if (INV && emb_truncates(mode)) {
+    if constexpr (K >= 6 && K <= 10)
+      if (args.m >= 2 * wsel<16>(K)) return launch_cols_inv2<F, K, 16, true>(fld, args, inst, st);
     return launch_cols<F, K, INV, 16, true>(fld, args, inst, st);
   }
   static const int use_inv2 = knob("INV2", 1);
