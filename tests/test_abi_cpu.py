@@ -245,3 +245,18 @@ def test_m31x2_premises():
     assert ei.value.code == -3
     assert fc.schedule(M31, 1 << 20) == (12, 8)
     assert lib.fcirc_matvec(M31, 1, 1, 2, 3, 1 << 25, 1, None) == -4   # above the maximum
+
+
+def test_synth_edge_mix_is_canonical_and_hits_the_corners():
+    """synth.edge_mix (the corner-biased parity inputs) draws canonical residues and covers the
+    carry/borrow corner values it names, for every field's modulus."""
+    import numpy as np
+    import synth
+    for p in [synth.P998, synth.P469, synth.P167, synth.GOLDILOCKS, (1 << 31) - 1]:
+        x = synth.edge_mix(p, (4, 4096), np.random.default_rng(5))
+        assert x.dtype == (np.uint32 if p < (1 << 32) else np.uint64)
+        v = x.astype(np.uint64)
+        assert int(v.max()) < p
+        for corner in (0, 1, p - 1, p - 2, (1 << 31) - 1):
+            if corner < p:
+                assert (v == corner).any(), (p, corner)
