@@ -270,6 +270,15 @@ template <class F, int M>
 static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
   // the application embeddings (fused path only) use one variant: the default R
   if (args.k == 0 && args.io.mode != EMB_PLAIN) return launch_block<F, M, RDefault<F>::RB, true>(fld, args, st);
+  // latency-bound small fused batches (C1: one 1024-point product): 4 elements per thread, i.e.
+  // more and shorter dependency chains (C1 7.5 -> 5.6 us per step, profiles/r01m_sweep_c1_small_r.txt)
+  if constexpr (M >= 8 && M <= 10) {
+    static const int rs = knob("SMALL_R", 4);
+    if (args.k == 0 && args.units <= 64) {
+      if (rs == 4) return launch_block<F, M, 4>(fld, args, st);
+      if (rs == 8) return launch_block<F, M, 8>(fld, args, st);
+    }
+  }
   if constexpr (M >= FTraits<F>::MMAX - 2) {
     static const int rb = knob(FTraits<F>::RB, RDefault<F>::RB);
     static const int rbf = knob(FTraits<F>::RBF, RDefault<F>::RBF);
