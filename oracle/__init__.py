@@ -10,6 +10,8 @@ Contents (each cites the PAPER.md line it follows, ``P:n``):
    with the row-vector identification: the C library ``liboracle.so``
   (``oracle.c``), O(n) per entry, exact 192-bit accumulation.
 * ``polymul_coeffs`` — schoolbook polynomial coefficients, C library.
+* ``fcirc_entries_batch`` / ``poly_eval_batch`` — the same definitions over a whole
+  ``[batch][n]`` array (per-instance index / point lists), threaded; indexing only.
 * ``bigint_mul``     — independent Karatsuba on 32-bit words, C library.
 * ``py_fcirc_matvec`` — second witness for ``fcirc_entries``: the same definition in
   arbitrary-precision Python ints (no ``%`` tricks), for small n.
@@ -63,6 +65,12 @@ def _load():
         lib.oracle_polymul_coeffs_m31x2.argtypes = [u64p, ctypes.c_int64, u64p, ctypes.c_int64, i64p, ctypes.c_int64,
                                                     u64p, ctypes.c_int]
         lib.oracle_bigint_mul_school.argtypes = [u32p, ctypes.c_int64, u32p, ctypes.c_int64, u32p]
+        lib.oracle_fcirc_entries_batch.argtypes = [ctypes.c_uint64, ctypes.c_uint64, u64p, u64p, ctypes.c_int64,
+                                                   ctypes.c_int64, i64p, ctypes.c_int64, u64p, ctypes.c_int]
+        lib.oracle_poly_eval_batch.argtypes = [ctypes.c_uint64, u64p, ctypes.c_int64, ctypes.c_int64, u64p,
+                                               ctypes.c_int64, u64p, ctypes.c_int]
+        lib.oracle_fcirc_entries_batch.restype = ctypes.c_int
+        lib.oracle_poly_eval_batch.restype = ctypes.c_int
         for fn in (lib.oracle_fcirc_entries, lib.oracle_polymul_coeffs, lib.oracle_bigint_mul,
                    lib.oracle_bigint_mul_school):
             fn.restype = ctypes.c_int
@@ -221,6 +229,77 @@ def eigen_check(p: int, n: int, f: int, a, b, c, thetas) -> bool:
     eb = poly_eval(p, b, thetas)
     ea = poly_eval(p, a, thi)
     return all(int(l) == int(x) * int(y) % p for l, x, y in zip(lhs, eb, ea))
+
+
+def fcirc_entries_batch(p: int, f: int, a, b, idx, threads: int | None = None) -> np.ndarray:
+    """``out[k, t] = (A_k b_k)_{idx[k, t]}`` for a batch (Definition 2 per instance).
+
+    ``a``, ``b``: ``[batch, n]`` residues; ``idx``: ``[batch, m]`` entry indices per instance.
+    """
+    lib = _load()
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.uint64))
+    idx = np.ascontiguousarray(np.asarray(idx, dtype=np.int64))
+    batch, n = a.shape
+    assert b.shape == a.shape and idx.ndim == 2 and idx.shape[0] == batch
+    out = np.zeros(idx.shape, dtype=np.uint64)
+    rc = lib.oracle_fcirc_entries_batch(int(p), int(f) % int(p), _ptr(a, ctypes.c_uint64), _ptr(b, ctypes.c_uint64),
+                                        n, batch, _ptr(idx, ctypes.c_int64), idx.shape[1],
+                                        _ptr(out, ctypes.c_uint64), threads or default_threads())
+    if rc != 0:
+        raise ValueError("oracle_fcirc_entries_batch: bad arguments")
+    return out
+
+
+def poly_eval_batch(p: int, c, xs, threads: int | None = None) -> np.ndarray:
+    """``out[k, t] = sum_i c[k, i] xs[k, t]^i mod p`` (Horner) for a batch of coefficient rows."""
+    lib = _load()
+    c = np.ascontiguousarray(np.asarray(c, dtype=np.uint64))
+    xs = np.ascontiguousarray(np.asarray(xs, dtype=np.uint64))   # reduced mod p in the C loop
+    batch, n = c.shape
+    assert xs.ndim == 2 and xs.shape[0] == batch
+    out = np.zeros(xs.shape, dtype=np.uint64)
+    rc = lib.oracle_poly_eval_batch(int(p), _ptr(c, ctypes.c_uint64), n, batch, _ptr(xs, ctypes.c_uint64),
+                                    xs.shape[1], _ptr(out, ctypes.c_uint64), threads or default_threads())
+    if rc != 0:
+        raise ValueError("oracle_poly_eval_batch: bad arguments")
+    return out
+
+
+def eigen_thetas_batch(p: int, n: int, w: int, batch: int, count: int, seed: int) -> np.ndarray:
+    """``[batch, count]`` seeded theta with theta^n f = 1 for f = w^n: theta =
+    w^-1 zeta_n^e with e drawn per instance."""
+    g = {998244353: 3, 469762049: 3, 167772161: 3, (1 << 64) - (1 << 32) + 1: 7}[int(p)]
+    z = pow(g, (p - 1) // n, p)
+    winv = pow(int(w), -1, p)
+    rng = np.random.default_rng(seed)
+    es = rng.integers(0, n, size=(batch, count))
+    zp = {}
+    out = np.zeros((batch, count), dtype=np.uint64)
+    for k in range(batch):
+        for t in range(count):
+            e = int(es[k, t])
+            if e not in zp:
+                zp[e] = winv * pow(z, e, p) % p
+            out[k, t] = zp[e]
+    return out
+
+
+def eigen_check_batch(p: int, n: int, f: int, a, b, c, thetas) -> np.ndarray:
+    """Per instance: all(sum_i c_i theta^i == (sum_j b_j theta^j)(sum_k a_k theta^-k)) over its row of
+    ``thetas`` (each with theta^n f = 1).  Returns a bool array [batch]."""
+    thetas = np.asarray(thetas, dtype=np.uint64)
+    for th in {int(t) for t in thetas.ravel()}:
+        assert pow(th, n, p) * f % p == 1
+    inv = {int(t): pow(int(t), -1, p) for t in set(thetas.ravel().tolist())}
+    thi = np.vectorize(lambda t: inv[int(t)], otypes=[np.uint64])(thetas)
+    lhs = poly_eval_batch(p, c, thetas)
+    eb = poly_eval_batch(p, b, thetas)
+    ea = poly_eval_batch(p, a, thi)
+    ok = np.ones(thetas.shape[0], dtype=bool)
+    for k in range(thetas.shape[0]):
+        ok[k] = all(int(l) == int(x) * int(y) % p for l, x, y in zip(lhs[k], eb[k], ea[k]))
+    return ok
 
 
 def bigint_mul(x, y, school: bool = False) -> np.ndarray:

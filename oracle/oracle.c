@@ -21,6 +21,11 @@
  *   oracle_fcirc_entries_m31x2, oracle_polymul_coeffs_m31x2
  *                          the same definitions over the paper's own ring Z/pZ[sqrt 3],
  *                          p = 2^31 - 1, elements packed u | v << 32.
+ *   oracle_fcirc_entries_batch, oracle_poly_eval_batch
+ *                          the same two definitions over a whole batch of instances (instance k of
+ *                          the caller's [batch][n] arrays with its own index / point list), threaded
+ *                          over (instance, index) pairs.  No new arithmetic: each element is
+ *                          fcirc_entry / the Horner loop above; only the indexing is batched.
  *   oracle_bigint_mul      product of two non-negative integers given as little-endian 32-bit
  *                          words (P:135-140 application): an independent Karatsuba recursion
  *                          (schoolbook below 32 words).  Exact, full product.
@@ -330,4 +335,69 @@ int oracle_polymul_coeffs_m31x2(const uint64_t* a, int64_t na, const uint64_t* b
   for (int64_t t = 0; t < nk; ++t) if (ks[t] < 0 || ks[t] > na + nb - 2) return -1;
   job_t J = {3, M31, 0, a, b, 0, na, nb, ks, out, 0, 0};
   return run_jobs(J, nk, threads);
+}
+
+/* ---------------- batched forms (indexing only; the arithmetic is fcirc_entry / Horner) ----------------
+ * Instance k uses a + k n, b + k n, its index list idx + k nidx and writes out + k nidx.  Work items
+ * (k, t) are split evenly across the threads. */
+typedef struct {
+  int kind;                 /* 0: fcirc entries, 1: Horner evaluation */
+  uint64_t p, f;
+  const uint64_t *a, *b;    /* kind 1: a = c, b unused */
+  int64_t n, per;           /* per = nidx (kind 0) or nx (kind 1) */
+  const int64_t* idx;
+  const uint64_t* xs;
+  uint64_t* out;
+  int64_t lo, hi;           /* flat work-item range [lo, hi) over batch * per */
+} bjob_t;
+
+static void* batch_worker(void* arg) {
+  bjob_t* J = (bjob_t*)arg;
+  for (int64_t w = J->lo; w < J->hi; ++w) {
+    const int64_t k = w / J->per;
+    if (J->kind == 0) {
+      J->out[w] = fcirc_entry(J->p, J->f, J->a + k * J->n, J->b + k * J->n, J->n, J->idx[w]);
+    } else {
+      const uint64_t* c = J->a + k * J->n;
+      u128 acc = 0, x = J->xs[w] % J->p;
+      for (int64_t i = J->n - 1; i >= 0; --i) acc = (acc * x + c[i]) % J->p;
+      J->out[w] = (uint64_t)acc;
+    }
+  }
+  return NULL;
+}
+
+static int run_batch(bjob_t proto, int64_t items, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  if (items < threads) threads = items > 0 ? (int)items : 1;
+  pthread_t th[256]; bjob_t jobs[256]; int made[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = proto;
+    jobs[t].lo = items * t / threads;
+    jobs[t].hi = items * (t + 1) / threads;
+  }
+  for (int t = 0; t < threads; ++t) {
+    made[t] = threads > 1 && pthread_create(&th[t], NULL, batch_worker, &jobs[t]) == 0;
+    if (!made[t]) batch_worker(&jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) if (made[t]) pthread_join(th[t], NULL);
+  return 0;
+}
+
+/* out[k][t] = (A_k b_k)_{idx[k][t]}: Definition 2 per instance, a, b: [batch][n] */
+int oracle_fcirc_entries_batch(uint64_t p, uint64_t f, const uint64_t* a, const uint64_t* b, int64_t n,
+                               int64_t batch, const int64_t* idx, int64_t nidx, uint64_t* out, int threads) {
+  if (!a || !b || !idx || !out || n < 1 || batch < 0 || nidx < 0 || p < 2) return -1;
+  for (int64_t t = 0; t < batch * nidx; ++t) if (idx[t] < 0 || idx[t] >= n) return -1;
+  bjob_t J = {0, p, f % p, a, b, n, nidx, idx, NULL, out, 0, 0};
+  return run_batch(J, batch * nidx, threads);
+}
+
+/* out[k][t] = sum_i c[k][i] xs[k][t]^i mod p (Horner), c: [batch][n], xs: [batch][nx] */
+int oracle_poly_eval_batch(uint64_t p, const uint64_t* c, int64_t n, int64_t batch, const uint64_t* xs, int64_t nx,
+                           uint64_t* out, int threads) {
+  if (!c || !xs || !out || n < 1 || batch < 0 || nx < 0 || p < 2) return -1;
+  bjob_t J = {1, p, 0, c, NULL, n, nx, NULL, xs, out, 0, 0};
+  return run_batch(J, batch * nx, threads);
 }

@@ -354,6 +354,73 @@ def test_eigen_check_detects_a_single_corrupted_entry():
     assert not oracle.eigen_check(p, n, f, a, b, c, th)
 
 
+def test_poly_eval_batch_vs_power_sums_and_closed_forms():
+    """Batched Horner (oracle_poly_eval_batch): per-instance rows and points.  Pinned by
+    x = 0 -> c_0, x = 1 -> sum c, x = -1 -> alternating sum, the geometric closed form
+    sum_{i<n} x^i = (x^n - 1)/(x - 1) on an all-ones row, and power sums with Python ints."""
+    rng = random.Random(16)
+    for p in [P998, GOLDILOCKS]:
+        batch, n = 5, 257
+        c = np.array([[rng.randrange(p) for _ in range(n)] for _ in range(batch)], dtype=np.uint64)
+        c[3, :] = 1
+        xs = np.array([[0, 1, p - 1, rng.randrange(2, p)] for _ in range(batch)], dtype=np.uint64)
+        got = oracle.poly_eval_batch(p, c, xs)
+        for k in range(batch):
+            row = [int(v) for v in c[k]]
+            assert int(got[k, 0]) == row[0]
+            assert int(got[k, 1]) == sum(row) % p
+            assert int(got[k, 2]) == sum(ci * (-1) ** i for i, ci in enumerate(row)) % p
+            x = int(xs[k, 3])
+            if k == 3:
+                assert int(got[k, 3]) == (pow(x, n, p) - 1) * pow(x - 1, -1, p) % p
+            assert int(got[k, 3]) == sum(ci * pow(x, i, p) for i, ci in enumerate(row)) % p
+
+
+def test_fcirc_entries_batch_indexing_and_closed_forms():
+    """The batched entry oracle uses instance k's own a, b and index row: pinned per instance by
+    the closed forms a = e_0 -> c = b and a = e_1 -> c = (b_1, .., b_{n-1}, f b_0) (Definition 2,
+    P:29-37) placed at different instances of one batch, and by the Python-int witness."""
+    rng = random.Random(17)
+    for p in [P998, GOLDILOCKS]:
+        n, batch = 24, 4
+        f = rng.randrange(1, p)
+        a = np.array([[rng.randrange(p) for _ in range(n)] for _ in range(batch)], dtype=np.uint64)
+        b = np.array([[rng.randrange(p) for _ in range(n)] for _ in range(batch)], dtype=np.uint64)
+        a[1, :] = 0
+        a[1, 0] = 1
+        a[2, :] = 0
+        a[2, 1] = 1
+        idx = np.array([rng.sample(range(n), 9) for _ in range(batch)], dtype=np.int64)
+        got = oracle.fcirc_entries_batch(p, f, a, b, idx)
+        bl = [[int(v) for v in row] for row in b]
+        shift = bl[2][1:] + [f * bl[2][0] % p]
+        for t in range(9):
+            assert int(got[1, t]) == bl[1][idx[1, t]]
+            assert int(got[2, t]) == shift[idx[2, t]]
+        for k in (0, 3):
+            full = oracle.py_fcirc_matvec(p, f, [int(v) for v in a[k]], bl[k])
+            assert [int(v) for v in got[k]] == [full[i] for i in idx[k]]
+
+
+def test_eigen_check_batch_flags_only_the_corrupted_instance():
+    rng = random.Random(18)
+    for p in [P998, GOLDILOCKS]:
+        n, batch = 32, 6
+        w = rng.randrange(1, p)
+        f = pow(w, n, p)
+        a = np.array([[rng.randrange(p) for _ in range(n)] for _ in range(batch)], dtype=np.uint64)
+        b = np.array([[rng.randrange(p) for _ in range(n)] for _ in range(batch)], dtype=np.uint64)
+        c = np.stack([oracle.fcirc_entries(p, f, a[k], b[k]) for k in range(batch)])
+        th = oracle.eigen_thetas_batch(p, n, w, batch, 16, seed=3)
+        for k in range(batch):
+            for t in th[k]:
+                assert pow(int(t), n, p) * f % p == 1
+        assert oracle.eigen_check_batch(p, n, f, a, b, c, th).all()
+        c[4, 9] = (int(c[4, 9]) + 1) % p
+        ok = oracle.eigen_check_batch(p, n, f, a, b, c, th)
+        assert not ok[4] and ok[[0, 1, 2, 3, 5]].all()
+
+
 def test_corollary1_embedding_any_n():
     """Corollary 1: for non-power-of-two n, the order-N circulant with row
     a' = (a_1..a_n, 0..0, a_2..a_n) times b' = (b, 0..0) has A b as its first n entries -- with the

@@ -1,0 +1,205 @@
+// gold_ab.cu — same-box A/B of Goldilocks arithmetic variants inside the real kernels (dev tool).
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o build/gold_ab tools/gold_ab.cu -lcuda
+//   build/gold_ab [reps]
+//
+// Each variant GV<V> overrides FieldGold's multiply / butterflies; k_block<GV<V>, 12, 8> (the C4 n = 2^20
+// sub-problem launch: 16384 units), k_cols_fwd2 and k_cols_inv2 (K = 8) run on the same random inputs
+// and twiddles; every variant's output must equal variant 0's bit for bit (all variants compute the
+// same canonical residues), and the per-launch time (CUDA events, median of reps) is printed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "../paper_2103_02605_b200/csrc/fcirc_kernels.cuh"
+
+namespace fcirc {
+
+template <int V>
+struct GV : FieldGold {
+  // reduce variants
+  __device__ __forceinline__ static uint64_t red(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    if constexpr (V == 0) {
+      return reduce4(t0, t1, t2, t3);
+    } else if constexpr (V == 2) {
+      uint32_t r0, r1;
+      // V2: V1's WIDE EPS product, canonicalisation as r + EPS with carry -> select
+      asm("{\n\t.reg .u32 c, m, h, s0, s1;\n\t.reg .u64 T, E, R;\n\t.reg .pred p;\n\t"
+          "mov.b64 T, {%2, %3};\n\t"
+          "mul.wide.u32 E, %4, 0xffffffff;\n\t"
+          "add.cc.u64 R, T, E;\n\t"
+          "addc.u32 c, 0, 0;\n\t"
+          "mov.b64 {%0, %1}, R;\n\t"
+          "sub.cc.u32      %0, %0, %5;\n\t"
+          "subc.cc.u32     %1, %1, 0;\n\t"
+          "subc.u32        c, c, 0;\n\t"
+          "neg.s32         m, c;\n\t"
+          "shr.s32         h, c, 31;\n\t"
+          "add.cc.u32      %0, %0, m;\n\t"
+          "addc.u32        %1, %1, h;\n\t"
+          "add.cc.u32      s0, %0, 0xffffffff;\n\t"
+          "addc.cc.u32     s1, %1, 0;\n\t"
+          "addc.u32        c, 0, 0;\n\t"
+          "setp.ne.u32     p, c, 0;\n\t"
+          "selp.b32        %0, s0, %0, p;\n\t"
+          "selp.b32        %1, s1, %1, p;\n\t"
+          "}"
+          : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+      return mk(r0, r1);
+    } else {
+      uint32_t r0, r1;
+      // V >= 1: t2 * EPS + (t1:t0) as one IMAD.WIDE.U32 with carry out (mul.wide + add.cc.u64)
+      asm("{\n\t.reg .u32 c, m, h;\n\t.reg .u64 T, E, R;\n\t.reg .pred p, q;\n\t"
+          "mov.b64 T, {%2, %3};\n\t"
+          "mul.wide.u32 E, %4, 0xffffffff;\n\t"
+          "add.cc.u64 R, T, E;\n\t"
+          "addc.u32 c, 0, 0;\n\t"
+          "mov.b64 {%0, %1}, R;\n\t"
+          "sub.cc.u32      %0, %0, %5;\n\t"
+          "subc.cc.u32     %1, %1, 0;\n\t"
+          "subc.u32        c, c, 0;\n\t"
+          "neg.s32         m, c;\n\t"
+          "shr.s32         h, c, 31;\n\t"
+          "add.cc.u32      %0, %0, m;\n\t"
+          "addc.u32        %1, %1, h;\n\t"
+          "setp.eq.u32     p, %1, 0xffffffff;\n\t"
+          "setp.ne.and.u32 q, %0, 0, p;\n\t"
+          "@q sub.u32      %0, %0, 1;\n\t"
+          "@q mov.u32      %1, 0;\n\t"
+          "}"
+          : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+      return mk(r0, r1);
+    }
+  }
+  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+    const uint64_t lo = a * b, hi = __umul64hi(a, b);
+    return red(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
+  __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(y, s); const uint64_t X = x; x = add_c(X, t); y = sub_c(X, t);
+  }
+  __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mul(x, s); const uint64_t Y = y; x = add_c(Y, t); y = sub_w(t, Y);
+  }
+  __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
+    const uint64_t s = add_c(u, v); const uint64_t d = sub_c(u, v); u = mul(s, si); v = d;
+  }
+  __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
+    const uint64_t s = add_c(u, v); const uint64_t d = sub_c(u, v); u = mul(s, si_k); v = mul(d, k);
+  }
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const { return mul(mul(a, b), k); }
+};
+
+}  // namespace fcirc
+
+using namespace fcirc;
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1); } } while (0)
+
+constexpr int L = 20, M = 12, K = L - M, R = 8, INST = 64;
+constexpr int64_t N = (int64_t)1 << L;
+constexpr int W = 8;   // wsel<8>(8)
+
+struct Bufs {
+  uint64_t *a, *b, *out, *ob, *twf, *twi;
+};
+
+template <class F>
+float time_launches(int reps, void (*launch)(const Bufs&, cudaStream_t), const Bufs& B) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  std::vector<float> t;
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaEventRecord(e0));
+    launch(B, 0);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms; CK(cudaEventElapsedTime(&ms, e0, e1)); t.push_back(ms);
+  }
+  std::sort(t.begin(), t.end());
+  return t[t.size() / 2];
+}
+
+template <int V>
+void run_block(const Bufs& B, cudaStream_t st) {
+  using F = GV<V>;
+  BlockArgs<F> ba{B.a, B.b, B.out, (int64_t)INST << K, K, B.twf, B.twi, 0, 0, EmbedIO{}};
+  auto kern = k_block<F, M, R, 1, 2, false, false>;
+  const size_t smem = 2 * (1 << M) * 8;
+  static bool once = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
+  (void)once;
+  kern<<<(unsigned)(INST << K), (1 << M) / R, smem, st>>>(F{}, ba);
+}
+template <int V>
+void run_fwd(const Bufs& B, cudaStream_t st) {
+  using F = GV<V>;
+  ColArgs<F> ca{B.a, B.b, B.out, B.ob, N >> K, N, 0, 0, B.twf, B.twi, 0, 0, EmbedIO{}};
+  ca.colblocks = ca.m / W;
+  ca.units = INST * ca.colblocks;
+  auto kern = k_cols_fwd2<F, K, R, W, 4, false>;
+  k_cols_fwd2<F, K, R, W, 4, false><<<(unsigned)ca.units, W * ((1 << K) / R), 2 * (1 << K) * W * 8, st>>>(F{}, ca);
+  (void)kern;
+}
+template <int V>
+void run_inv(const Bufs& B, cudaStream_t st) {
+  using F = GV<V>;
+  ColArgs<F> ca{B.a, nullptr, B.out, nullptr, N >> K, N, 0, 0, B.twf, B.twi, 12345, 678, EmbedIO{}};
+  ca.colblocks = ca.m / (2 * W);
+  ca.units = INST * ca.colblocks;
+  k_cols_inv2<F, K, R, W, 4, false><<<(unsigned)ca.units, W * ((1 << K) / R), 2 * (1 << K) * W * 8, st>>>(F{}, ca);
+}
+
+template <int V>
+void bench(const char* name, int reps, const Bufs& B, std::vector<uint64_t>* ref_blk, std::vector<uint64_t>* ref_fwd,
+           std::vector<uint64_t>* ref_inv) {
+  const size_t ne = (size_t)INST * N;
+  std::vector<uint64_t> h(ne), h2(ne);
+  float tb = time_launches<GV<V>>(reps, run_block<V>, B);
+  CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
+  bool okb = ref_blk->empty() ? (*ref_blk = h, true) : (*ref_blk == h);
+  float tf = time_launches<GV<V>>(reps, run_fwd<V>, B);
+  CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(h2.data(), B.ob, ne * 8, cudaMemcpyDeviceToHost));
+  h.insert(h.end(), h2.begin(), h2.end());
+  bool okf = ref_fwd->empty() ? (*ref_fwd = h, true) : (*ref_fwd == h);
+  float ti = time_launches<GV<V>>(reps, run_inv<V>, B);
+  h.resize(ne);
+  CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
+  bool oki = ref_inv->empty() ? (*ref_inv = h, true) : (*ref_inv == h);
+  printf("{\"variant\": %d, \"name\": \"%s\", \"k_block_ms\": %.4f, \"k_cols_fwd2_ms\": %.4f, \"k_cols_inv2_ms\": %.4f, "
+         "\"sum_ms\": %.4f, \"match\": [%d, %d, %d]}\n", V, name, tb, tf, ti, tb + tf + ti, okb, okf, oki);
+  fflush(stdout);
+}
+
+int main(int argc, char** argv) {
+  const int reps = argc > 1 ? atoi(argv[1]) : 20;
+  const size_t ne = (size_t)INST * N;
+  const uint64_t P = FieldGold::P;
+  std::mt19937_64 rng(2103);
+  std::vector<uint64_t> h(ne);
+  Bufs B;
+  CK(cudaMalloc(&B.a, ne * 8)); CK(cudaMalloc(&B.b, ne * 8)); CK(cudaMalloc(&B.out, ne * 8)); CK(cudaMalloc(&B.ob, ne * 8));
+  for (auto& x : h) x = rng() % P;
+  CK(cudaMemcpy(B.a, h.data(), ne * 8, cudaMemcpyHostToDevice));
+  for (auto& x : h) x = rng() % P;
+  CK(cudaMemcpy(B.b, h.data(), ne * 8, cudaMemcpyHostToDevice));
+  std::vector<uint64_t> tw(N);
+  CK(cudaMalloc(&B.twf, N * 8)); CK(cudaMalloc(&B.twi, N * 8));
+  for (auto& x : tw) x = rng() % P;
+  CK(cudaMemcpy(B.twf, tw.data(), N * 8, cudaMemcpyHostToDevice));
+  for (auto& x : tw) x = rng() % P;
+  CK(cudaMemcpy(B.twi, tw.data(), N * 8, cudaMemcpyHostToDevice));
+  // opt-in smem for the fwd/inv kernels (32 KB: not needed) -- k_block needs 64 KB
+  std::vector<uint64_t> rb, rf, ri;
+  for (int round = 0; round < 2; ++round) {   // two rounds: A B A B
+    bench<0>("current", reps, B, &rb, &rf, &ri);
+    bench<1>("wide-eps reduce", reps, B, &rb, &rf, &ri);
+    bench<2>("wide-eps reduce, carry-select canonicalisation", reps, B, &rb, &rf, &ri);
+  }
+  return 0;
+}
