@@ -39,16 +39,15 @@ import synth  # noqa: E402
 METRIC = "f-circulant matvec Gelem/s mod p at n=2^20 (batched); % of HBM/int roofline"
 UNIT = "Gelem/s"
 
-# Roofline denominators.  Integer pipe: derived from the unit counts measured on
-# this pool's B200 (profiles/r01_peaks.jsonl: IMAD 64/clk/SM, IMAD.HI and IMAD.WIDE.U32 32/clk/SM,
-# i.e. 2 FMA-pipe slots each) and the SM clock of MEASURED_PEAKS.json (1965 MHz), 148 SMs:
-#   Goldilocks modmul: minimum 4 IMAD.WIDE partial products = 8 slots -> 8 modmul/clk/SM
-#   32-bit Shoup modmul: 1 IMAD.HI + 2 IMAD = 4 slots                 -> 16 modmul/clk/SM
-SMS = 148
-SM_MHZ = 1965.0
-MODMUL_PER_CLK_SM = {"u64": 8.0, "u32": 16.0}
-PRIMITIVE_MEASURED_PER_CLK_SM = {"u64": 3.16, "u32": 15.98}  # profiles/r01_peaks.jsonl (gold64 / shoup32)
+# Roofline denominators are MEASURED in the same run: the integer peak is the rate of the
+# library's own ring primitives (fcirc_primitive_rate: SURVEY §8(d)'s R_const / R_var), the
+# multiplier-only ceiling is derived from the raw IMAD.WIDE.U32 rate measured beside it, and HBM is
+# MEASURED_PEAKS.json's copy bandwidth (driver-written).
 HBM_GBS_FALLBACK = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+# primitive kinds per element width: (R_const probe, R_var probe, IMAD.WIDE slots per modmul)
+PRIMS = {"u64": ("gold_mul", "gold_mul", 4), "u32": ("u32_mulc", "u32_leaf", 2), "fp2": ("m31x2_mul", "m31x2_mul", 4)}
+PROBE_ITERS = {"gold_mul": 20000, "u32_mulc": 60000, "u32_leaf": 40000, "m31x2_mul": 30000, "imad_wide": 100000,
+               "gold_fwd_a": 15000, "gold_fwd_b": 15000, "gold_inv": 15000, "u32_fwd_a": 40000}
 
 WORKLOADS = {
     "C4_n20": "C4 @ n=2^20: Goldilocks f-circulant matvec, batch 64, f=w^n",
@@ -181,20 +180,44 @@ def whole_job_gelems(world: int, batch: int, n: int, steps: int, ms_max: float) 
     return world * batch * n * steps / (ms_max * 1e-3) / 1e9
 
 
-def algorithmic_modmuls(kind: str, n: int, batch: int, M: int, K: int) -> float:
-    """Algorithmic modmuls per step attributed to one kernel kind:
+def algorithmic_modmuls(kind: str, n: int, batch: int, M: int, K: int):
+    """(M_const, M_var) algorithmic modmuls per step attributed to one kernel kind:
     M_const = 1.5 n L (0.5 n L each for the a split, the b split, the recombination), M_var = n.
     (M, K) = the library's pass schedule (fcirc_schedule): sub-problems of 2^M, K column levels."""
     L = n.bit_length() - 1
     if kind == "k_block_fused":
-        return batch * n * (1.5 * L + 1)
+        return batch * n * 1.5 * L, batch * n
     if kind == "k_block_sub":
-        return batch * n * (1.5 * M + 1)
+        return batch * n * 1.5 * M, batch * n
     if kind == "k_cols_fwd":
-        return batch * n * 1.0 * K
+        return batch * n * 1.0 * K, 0.0
     if kind == "k_cols_inv":
-        return batch * n * 0.5 * K
-    return 0.0
+        return batch * n * 0.5 * K, 0.0
+    return 0.0, 0.0
+
+
+def measure_primitives(fc, width: str, sampler_cls, device: int) -> dict:
+    """Rates of the library's own primitives on this GPU, now (fcirc_primitive_rate), with the SM clock
+    sampled while they run: R_const, R_var and the IMAD.WIDE.U32 rate for the ceiling."""
+    rc_kind, rv_kind, slots = PRIMS[width]
+    kinds = sorted({rc_kind, rv_kind, "imad_wide"} |
+                   ({"gold_fwd_a", "gold_fwd_b", "gold_inv"} if width == "u64" else
+                    {"u32_fwd_a"} if width == "u32" else set()))
+    out = {}
+    smp = sampler_cls(device)
+    with smp:
+        for k in kinds:
+            fc.primitive_rate(k, max(1000, PROBE_ITERS[k] // 10))      # warm the clocks
+            ops, ms = fc.primitive_rate(k, PROBE_ITERS[k])
+            out[k] = {"ops_per_s": ops, "ms": ms}
+    clk = smp.summary()
+    mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0
+    for k, v in out.items():
+        v["per_clk_per_sm"] = v["ops_per_s"] / (148 * mhz * 1e6)
+    return {"R_const": out[rc_kind]["ops_per_s"], "R_var": out[rv_kind]["ops_per_s"],
+            "R_const_kind": rc_kind, "R_var_kind": rv_kind,
+            "ceiling_modmul_per_s": out["imad_wide"]["ops_per_s"] / slots, "imad_wide_slots_per_modmul": slots,
+            "primitives": out, "clocks": clk}
 
 
 def cfg_dtype(p: int) -> str:
@@ -379,6 +402,46 @@ def run_reference(args):
     return 0
 
 
+def prim_width(p: int) -> str:
+    return "fp2" if p == synth.M31X2 else ("u64" if p >= (1 << 32) else "u32")
+
+
+def bench_parity(wl, out, thetas: int, instances: int) -> dict:
+    """Check the product the timed region computed (the last step's output, copied back) against the
+    oracle: >= 1024 seeded entries + boundary on `instances` spread
+    instances, the eigen-checksum at `thetas` theta on EVERY instance (matvec); seeded coefficients
+    + Schwartz-Zippel (polymul); every full product vs Python ints (bigint).  Test infrastructure
+    (tests/parity.py -> oracle/), run after timing."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import parity
+    t0 = time.time()
+    host = out.cpu().numpy()
+    i = wl.inp
+    if wl.kind == "matvec":
+        ks = np.unique(np.linspace(0, wl.batch - 1, min(instances, wl.batch)).astype(np.int64))
+        sub = dict(i, a=i["a"][ks], b=i["b"][ks], batch=len(ks))
+        r1 = parity.check_matvec(wl.name + "[bench sampled]", sub, host[ks], full=False, thetas=0)
+        r2 = parity.check_matvec(wl.name + "[bench checksums]", i, host, full=False, sample=0, thetas=thetas)
+        return {"sampled_instances": int(len(ks)), "entries": r1["entries"], "eigen_instances": wl.batch,
+                "thetas_per_instance": thetas, "mismatches": r1["mismatches"] + r2["mismatches"],
+                "eigen_ok": r2["eigen_ok"], "seconds": round(time.time() - t0, 2)}
+    if wl.kind == "polymul":
+        ks = np.unique(np.linspace(0, wl.batch - 1, min(instances, wl.batch)).astype(np.int64))
+        sub = dict(i, a=i["a"][ks], b=i["b"][ks], batch=len(ks))
+        r = parity.check_polymul(wl.name + "[bench]", sub, host[ks])
+        return {"sampled_instances": int(len(ks)), "entries": r["entries"], "sz_points_per_instance":
+                r["sz_points_per_instance"], "mismatches": r["mismatches"], "seconds": round(time.time() - t0, 2)}
+    bad = 0
+    for k in range(wl.batch):
+        z = int.from_bytes(np.ascontiguousarray(host[k], dtype="<u4").tobytes(), "little")
+        x = int.from_bytes(np.ascontiguousarray(i["x"][k], dtype="<u4").tobytes(), "little")
+        y = int.from_bytes(np.ascontiguousarray(i["y"][k], dtype="<u4").tobytes(), "little")
+        bad += z != x * y
+    assert bad == 0, f"bigint parity: {bad} wrong products"
+    return {"instances": wl.batch, "entries": int(host.size), "mode": "every full product vs Python int",
+            "mismatches": int(bad), "seconds": round(time.time() - t0, 2)}
+
+
 def run_fcirc(args):
     import torch
     import torch.distributed as dist
@@ -418,8 +481,10 @@ def run_fcirc(args):
         graph.replay()
         torch.cuda.synchronize()
 
-    # ---- timed region (device time, CUDA events on the launching stream)
+    # ---- timed region (device time, CUDA events on the launching stream; one event pair per step
+    # for the min / median, one pair around all K steps for the mean)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches = 0
     if world > 1:
         dist.barrier()
@@ -428,11 +493,13 @@ def run_fcirc(args):
     fc.profile_enable(not use_graph)
     with sampler:
         ev0.record(stream)
-        for _ in range(args.steps):
+        for k in range(args.steps):
+            sev[k][0].record(stream)
             if use_graph:
                 graph.replay()
             else:
                 launches += wl.step()
+            sev[k][1].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     fc.profile_enable(False)
@@ -446,38 +513,61 @@ def run_fcirc(args):
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
+    step_ms = sorted(a.elapsed_time(b) for a, b in sev)
     ms_max = max_over_ranks(ms, world)
     ms_step = ms_max / args.steps
+    ms_min = max_over_ranks(step_ms[0], world)
+    ms_median = max_over_ranks(statistics.median(step_ms), world)
     value = world * wl.elems * args.steps / (ms_max * 1e-3) / 1e9
 
+    # ---- parity of the benched product (after timing; the output of the last timed step)
+    parity_blk = None
+    if not args.no_parity:
+        parity_blk = bench_parity(wl, wl.out, thetas=args.parity_thetas, instances=4)
+
+    # ---- measured integer peaks (same run, same GPU): the library's own primitives
+    width, pw, n, batch = wl.width, prim_width(wl.p), wl.mm_n, wl.mm_batch
+    prims = measure_primitives(fc, pw, ClockSampler, torch.cuda.current_device())
+    R_const, R_var, R_ceil = prims["R_const"], prims["R_var"], prims["ceiling_modmul_per_s"]
+
     # ---- roofline of the dominant kernel
-    width, n, batch = wl.width, wl.mm_n, wl.mm_batch
     dom = max((k for k in prof if prof[k][0] > 0), key=lambda k: prof[k][1])
     cnt, kms = prof[dom]
     sub_log, top = fc.schedule(wl.p, n)
-    per_launch_mm = algorithmic_modmuls(dom, n, batch, sub_log, top) * args.steps / cnt
+    mc, mv = algorithmic_modmuls(dom, n, batch, sub_log, top)
+    mc, mv = mc * args.steps / cnt, mv * args.steps / cnt          # per launch
     avg_ms = kms / cnt
-    achieved = per_launch_mm / (avg_ms * 1e-3) / 1e12
-    peak = SMS * SM_MHZ * 1e6 * MODMUL_PER_CLK_SM[width] / 1e12
+    achieved = (mc + mv) / (avg_ms * 1e-3) / 1e12
+    t_roof_k = mc / R_const + mv / R_var                           # seconds at the measured peak
+    peak = (mc + mv) / t_roof_k / 1e12
+    peak_ceil = R_ceil / 1e12
     mp = measured_peaks()
     hbm = (mp or {}).get("hbm_gbs", HBM_GBS_FALLBACK)
     L = n.bit_length() - 1
-    step_mm = batch * n * (1.5 * L + 1)
+    step_mc, step_mv = batch * n * 1.5 * L, batch * n
     step_bytes = 3 * batch * n * (8 if width == "u64" else 4)
-    t_roof = max(step_bytes / (hbm * 1e9), step_mm / (peak * 1e12))
+    t_int = step_mc / R_const + step_mv / R_var
+    t_roof = max(step_bytes / (hbm * 1e9), t_int)
     tr = traffic_record(args.config, dom)
     roofline = {
         "bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "Tmodmul/s",
         "frac": achieved / peak, "traffic": tr["bytes_per_launch"] if tr else None,
         "traffic_source": (f"{tr['report']} ({tr['note']})" if tr else None),
-        "per_launch": {"modmuls": per_launch_mm, "avg_ms": avg_ms, "launches": cnt},
-        "peak_derivation": f"{SMS} SMs x {SM_MHZ:.0f} MHz x {MODMUL_PER_CLK_SM[width]:.0f} modmul/clk/SM "
-                           f"(minimal FMA-pipe slots per modmul, DESIGN.md §6); of derived peak",
-        "primitive_microbench_tmodmul_s": SMS * SM_MHZ * 1e6 * PRIMITIVE_MEASURED_PER_CLK_SM[width] / 1e12,
+        "peak_source": (f"measured in this run: fcirc_primitive_rate {prims['R_const_kind']} (R_const) / "
+                        f"{prims['R_var_kind']} (R_var), the library's own modmul primitives on all SMs "
+                        f"(SURVEY §8(d)); blended for this kernel's const/var mix"),
+        "ceiling": peak_ceil, "frac_vs_ceiling": achieved / peak_ceil,
+        "ceiling_source": (f"measured IMAD.WIDE.U32 rate / {prims['imad_wide_slots_per_modmul']} "
+                           f"(multiplier-only: the minimum multiply issue slots of one modmul, DESIGN.md §6)"),
+        "per_launch": {"modmuls_const": mc, "modmuls_var": mv, "avg_ms": avg_ms, "launches": cnt},
+        "primitives": {k: {"tops_per_s": v["ops_per_s"] / 1e12, "per_clk_per_sm": v["per_clk_per_sm"]}
+                       for k, v in prims["primitives"].items()},
+        "primitive_clocks": prims["clocks"],
         "kernel_share_of_step": kms / ms,
         "kernels": {k: {"launches": v[0], "ms_total": v[1]} for k, v in prof.items() if v[0]},
         "step": {"t_roof_ms": 1000 * t_roof, "frac": 1000 * t_roof / ms_step,
-                 "hbm_bound_ms": 1000 * step_bytes / (hbm * 1e9), "alu_bound_ms": 1000 * step_mm / (peak * 1e12),
+                 "frac_vs_ceiling": 1000 * max(step_bytes / (hbm * 1e9), (step_mc + step_mv) / R_ceil) / ms_step,
+                 "hbm_bound_ms": 1000 * step_bytes / (hbm * 1e9), "alu_bound_ms": 1000 * t_int,
                  "hbm_gbs_peak": hbm, "hbm_peak_source": "MEASURED_PEAKS.json hbm_gbs" if mp else "fallback",
                  "hbm_gbs_achieved_alg": step_bytes / (ms_step * 1e-3) / 1e9},
     }
@@ -508,11 +598,13 @@ def run_fcirc(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "ms_min": ms_min, "ms_median": ms_median,
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": width, "data": "synthetic (seeded uniform residues, SURVEY §8(d))",
             "config": wl.config_block(args), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": sampler.summary(), "plan_build_ms": plan_ms,
-            "timing": "CUDA graph replay of the step" if use_graph else "API call per step",
+            "parity": parity_blk, "gpu_launches": launches, "clocks": sampler.summary(), "plan_build_ms": plan_ms,
+            "timing": ("CUDA graph replay of the step" if use_graph else "API call per step") +
+                      "; ms_per_step = mean over the K steps (one event pair), ms_min / ms_median over per-step event pairs",
         }
         if wl.kind in ("polymul", "bigint"):
             line["products_per_s"] = world * wl.batch * args.steps / (ms_max * 1e-3)
@@ -533,6 +625,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-parity", action="store_true", help="skip the oracle check of the benched output")
+    ap.add_argument("--parity-thetas", type=int, default=4,
+                    help="eigen-checksum points per instance in the bench parity check")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay a CUDA graph of one step in the timed region "
                          "(auto: launch-bound steps -- fewer than 2^20 elements, or the 14-launch bigint)")

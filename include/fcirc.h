@@ -30,8 +30,14 @@
  *  - Thread safety: calls may be made concurrently from several host threads; the plan cache is
  *    mutex-guarded (LRU, at most 64 plans / 2 GiB of tables).  Scratch memory is allocated
  *    stream-ordered from the device's default memory pool (cudaMallocAsync / cudaFreeAsync on
- *    `stream`), so concurrent calls on different streams never share it and a call can be
- *    captured into a CUDA graph once its plan exists (first call for (p, f, n) outside capture).
+ *    `stream`), so concurrent calls on different streams never share it.
+ *  - CUDA graphs: a call can be captured into a graph once its plan exists (the first call for a
+ *    (device, p, f, n) must happen outside capture; inside a capture it returns FCIRC_EINVAL).  A
+ *    plan used during a capture is pinned in the cache -- never evicted -- so the graph may be
+ *    replayed at any later time; fcirc_release_cache drops pinned plans too, after which such
+ *    graphs must not be replayed.  Evicted (unpinned) plans free their tables stream-ordered after
+ *    every recorded use has completed (no device-wide synchronisation, safe during other threads'
+ *    captures).
  *  - Nothing here ever falls back to a CPU implementation.
  */
 #ifndef FCIRC_H
@@ -69,7 +75,8 @@ extern "C" {
  *   f      the scalar of the f-circulant, reduced mod p by the library
  *   a      [batch][n] first rows (device)          b  [batch][n] vectors (device)
  *   c      [batch][n] results (device); must not overlap a or b
- *   n      matrix order, power of two, 1 <= n <= 2^23 (uint32 primes, also n | p-1) or 2^22 (Goldilocks)
+ *   n      matrix order, power of two with n | p-1: 1 <= n <= 2^23 for 998244353 (its 2-adicity), 2^24 for
+ *          469762049, 167772161, Goldilocks and Z/(2^31-1)[sqrt 3] (2^12..2^13-point sub-problems x 2^11 column levels)
  *   batch  number of independent instances, >= 1 (all share p, f, n)
  *   stream cudaStream_t
  * Errors: FCIRC_EINVAL, FCIRC_EPRIME, FCIRC_ESIZE, FCIRC_ENOROOT, FCIRC_ENOMEM, FCIRC_ECUDA.
@@ -174,8 +181,40 @@ int fcirc_plan_table(uint64_t p, uint64_t f, int64_t n, uint64_t* s, uint64_t* s
 int fcirc_profile_enable(int on);
 int fcirc_profile_read(int64_t* counts, double* ms, int nkinds);
 
+/*
+ * fcirc_primitive_rate — measured integer throughput of the product's OWN ring primitives (the
+ * FieldGold / FieldU32 functions the kernels inline), for the roofline's integer peak (SURVEY
+ * §8(d): R_const, R_var measured in a register-resident all-SM microbenchmark).
+ * One warm-up and one timed launch on `stream` (CUDA events; synchronises the stream): every SM at
+ * full occupancy, 8 independent dependency chains per thread, `iters` iterations per chain.
+ *   kind  FCIRC_PRIM_*:
+ *           GOLD_MUL    Goldilocks 64x64 -> canonical modmul (const x var and var x var: one function)
+ *           GOLD_FWD_A / GOLD_FWD_B / GOLD_INV  the three Goldilocks butterflies (1 modmul each)
+ *           U32_MULC    Shoup const x var modmul (p = 998244353)
+ *           U32_LEAF    Montgomery var x var modmul
+ *           U32_FWD_A   the 32-bit row butterfly (1 modmul)
+ *           IMAD_WIDE   raw 32x32+64 -> 64 multiply-adds (the multiplier-only ceiling: a Goldilocks
+ *                       modmul needs >= 4, a Shoup modmul the issue slots of 2)
+ *           M31X2_MUL   product in the paper's ring Z/(2^31-1)[sqrt 3]
+ *   *ops_per_s  primitives per second;  *ms  the timed launch (may be NULL)
+ * Errors: FCIRC_EINVAL (unknown kind, iters < 1, null ops_per_s), FCIRC_ENOMEM, FCIRC_ECUDA.
+ */
+#define FCIRC_PRIM_GOLD_MUL 0
+#define FCIRC_PRIM_GOLD_FWD_A 1
+#define FCIRC_PRIM_GOLD_FWD_B 2
+#define FCIRC_PRIM_GOLD_INV 3
+#define FCIRC_PRIM_U32_MULC 4
+#define FCIRC_PRIM_U32_LEAF 5
+#define FCIRC_PRIM_U32_FWD_A 6
+#define FCIRC_PRIM_IMAD_WIDE 7
+#define FCIRC_PRIM_M31X2_MUL 8
+int fcirc_primitive_rate(int kind, int64_t iters, double* ops_per_s, double* ms, void* stream);
+
 /* release all cached plans and trim the current device's default memory pool (tests / teardown) */
 int fcirc_release_cache(void);
+
+/* number of cached plans (all devices); *pinned (may be NULL) = how many are pinned by graph captures */
+int64_t fcirc_plan_count(int* pinned);
 
 #ifdef __cplusplus
 }

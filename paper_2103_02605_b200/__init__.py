@@ -11,6 +11,8 @@ Functions mirror the C ABI names:
   polymul(a, b, p, out=None)        -> fcirc_polymul      (device tensors [batch, na], [batch, nb])
   bigint_mul(x, y, out=None)        -> bigint_mul         (device uint32 words [batch, nx], [batch, ny])
   plan_table(p, f, n)               -> fcirc_plan_table   (host-only twist-table inspection)
+  primitive_rate(kind)              -> fcirc_primitive_rate (measured rate of the ring primitives)
+  plan_count()                      -> fcirc_plan_count   (cached / graph-pinned plans)
 """
 from __future__ import annotations
 
@@ -20,7 +22,7 @@ import os
 import numpy as np
 
 __all__ = ["FcircError", "matvec", "matvec_host", "circulant_matvec", "polymul", "bigint_mul", "plan_table", "strerror",
-           "last_launch_count", "release_cache", "version", "library_path", "schedule", "P998", "P469", "P167",
+           "last_launch_count", "release_cache", "plan_count", "primitive_rate", "version", "library_path", "schedule", "P998", "P469", "P167",
            "GOLDILOCKS", "PRIMES", "M31X2", "fp2_pack"]
 
 P998 = 998244353
@@ -71,6 +73,11 @@ def _load():
     lib.fcirc_schedule.argtypes = [u64, i64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
     lib.fcirc_profile_enable.argtypes = [ctypes.c_int]
     lib.fcirc_profile_read.argtypes = [vp, vp, ctypes.c_int]
+    lib.fcirc_primitive_rate.argtypes = [ctypes.c_int, i64, ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double), vp]
+    lib.fcirc_primitive_rate.restype = ctypes.c_int
+    lib.fcirc_plan_count.argtypes = [ctypes.POINTER(ctypes.c_int)]
+    lib.fcirc_plan_count.restype = i64
     for fn in (lib.fcirc_matvec, lib.fcirc_matvec_host, lib.fcirc_circulant_matvec, lib.fcirc_polymul, lib.bigint_mul, lib.fcirc_plan_table,
                lib.fcirc_schedule,
                lib.fcirc_release_cache, lib.fcirc_profile_enable, lib.fcirc_profile_read):
@@ -117,6 +124,30 @@ def release_cache() -> None:
     _load().fcirc_release_cache()
 
 
+def plan_count():
+    """(cached plans, of which pinned by CUDA-graph captures) -- fcirc_plan_count."""
+    pinned = ctypes.c_int(0)
+    n = _load().fcirc_plan_count(ctypes.byref(pinned))
+    return int(n), int(pinned.value)
+
+
+PRIMITIVES = {"gold_mul": 0, "gold_fwd_a": 1, "gold_fwd_b": 2, "gold_inv": 3, "u32_mulc": 4, "u32_leaf": 5,
+              "u32_fwd_a": 6, "imad_wide": 7, "m31x2_mul": 8}
+
+
+def primitive_rate(kind: str, iters: int = 20000, stream=None):
+    """(primitives per second, ms of the timed launch) of one of the library's own ring primitives
+    on all SMs of the current device (fcirc_primitive_rate; synchronises the stream)."""
+    torch = _torch()
+    ops = ctypes.c_double(0.0)
+    ms = ctypes.c_double(0.0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rc = _load().fcirc_primitive_rate(PRIMITIVES[kind], int(iters), ctypes.byref(ops), ctypes.byref(ms),
+                                      _stream_handle(stream, dev))
+    _check(rc, "fcirc_primitive_rate")
+    return float(ops.value), float(ms.value)
+
+
 def _check(rc: int, where: str):
     if rc != 0:
         raise FcircError(rc, where)
@@ -147,9 +178,29 @@ def _dev_tensor(x, p: int, name: str):
     return x
 
 
-def _stream_handle(stream):
+def _same_device(ref, *others):
+    for name, x in others:
+        if x.device != ref.device:
+            raise ValueError(f"{name} is on {x.device}, expected {ref.device} (all operands on one GPU)")
+
+
+def _check_out(out, shape, p: int, name: str = "out"):
+    _dev_tensor(out, p, name)
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    return out
+
+
+def _stream_handle(stream, device):
+    """The stream the library launches on: the given one (must belong to `device`) or `device`'s
+    current stream."""
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
+    if stream is None:
+        s = torch.cuda.current_stream(device)
+    else:
+        s = stream
+        if s.device != device:
+            raise ValueError(f"stream belongs to {s.device}, operands to {device}")
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -169,9 +220,11 @@ def matvec(a, b, f: int, p: int, out=None, stream=None):
     batch = a.numel() // n if n else 0
     if out is None:
         out = torch.empty_like(a)
-    _dev_tensor(out, p, "out")
-    rc = _load().fcirc_matvec(int(p), _scalar(f, p), a.data_ptr(), b.data_ptr(), out.data_ptr(), n, batch,
-                              _stream_handle(stream))
+    _check_out(out, a.shape, p)
+    _same_device(a, ("b", b), ("out", out))
+    with torch.cuda.device(a.device):   # the library launches on the current device
+        rc = _load().fcirc_matvec(int(p), _scalar(f, p), a.data_ptr(), b.data_ptr(), out.data_ptr(), n, batch,
+                                  _stream_handle(stream, a.device))
     _check(rc, "fcirc_matvec")
     return out
 
@@ -190,9 +243,11 @@ def circulant_matvec(a, b, p: int, out=None, stream=None):
     batch = a.numel() // n if n else 0
     if out is None:
         out = torch.empty_like(a)
-    _dev_tensor(out, p, "out")
-    rc = _load().fcirc_circulant_matvec(int(p), a.data_ptr(), b.data_ptr(), out.data_ptr(), n, batch,
-                                        _stream_handle(stream))
+    _check_out(out, a.shape, p)
+    _same_device(a, ("b", b), ("out", out))
+    with torch.cuda.device(a.device):
+        rc = _load().fcirc_circulant_matvec(int(p), a.data_ptr(), b.data_ptr(), out.data_ptr(), n, batch,
+                                            _stream_handle(stream, a.device))
     _check(rc, "fcirc_circulant_matvec")
     return out
 
@@ -219,6 +274,8 @@ def matvec_host(a, b, f: int, p: int, out=None):
     if out is None:
         out = np.empty(sa, dtype=np.uint64 if _elem_bytes(p) == 8 else np.uint32)
     pc, sc = _host_ptr(out, p, "out")
+    if tuple(sc) != tuple(sa):
+        raise ValueError(f"out has shape {tuple(sc)}, expected {tuple(sa)}")
     n = sa[-1]
     batch = int(np.prod(sa)) // n
     rc = _load().fcirc_matvec_host(int(p), _scalar(f, p), pa, pb, pc, n, batch)
@@ -237,9 +294,11 @@ def polymul(a, b, p: int, out=None, stream=None):
         raise ValueError("a and b must have the same batch")
     if out is None:
         out = torch.empty((*a.shape[:-1], na + nb - 1), dtype=a.dtype, device=a.device)
-    _dev_tensor(out, p, "out")
-    rc = _load().fcirc_polymul(int(p), a.data_ptr(), na, b.data_ptr(), nb, out.data_ptr(), batch,
-                               _stream_handle(stream))
+    _check_out(out, (*a.shape[:-1], na + nb - 1), p)
+    _same_device(a, ("b", b), ("out", out))
+    with torch.cuda.device(a.device):
+        rc = _load().fcirc_polymul(int(p), a.data_ptr(), na, b.data_ptr(), nb, out.data_ptr(), batch,
+                                   _stream_handle(stream, a.device))
     _check(rc, "fcirc_polymul")
     return out
 
@@ -255,8 +314,11 @@ def bigint_mul(x, y, out=None, stream=None):
         raise ValueError("x and y must have the same batch")
     if out is None:
         out = torch.empty((*x.shape[:-1], nx + ny), dtype=x.dtype, device=x.device)
-    _dev_tensor(out, P998, "out")
-    rc = _load().bigint_mul(x.data_ptr(), nx, y.data_ptr(), ny, out.data_ptr(), batch, _stream_handle(stream))
+    _check_out(out, (*x.shape[:-1], nx + ny), P998)
+    _same_device(x, ("y", y), ("out", out))
+    with torch.cuda.device(x.device):
+        rc = _load().bigint_mul(x.data_ptr(), nx, y.data_ptr(), ny, out.data_ptr(), batch,
+                                _stream_handle(stream, x.device))
     _check(rc, "bigint_mul")
     return out
 

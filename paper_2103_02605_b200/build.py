@@ -15,7 +15,7 @@ LIB_DIR = os.path.join(HERE, "lib")
 OBJ_DIR = os.path.join(LIB_DIR, "obj")
 LIB = os.path.join(LIB_DIR, "libfcirc.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-SOURCES = ["matvec_gold.cu", "matvec_u32.cu", "matvec_m31.cu", "api.cu", "plan.cpp"]
+SOURCES = ["matvec_gold.cu", "matvec_u32.cu", "matvec_m31.cu", "api.cu", "plan.cpp", "probe.cu"]
 HEADERS = ["modarith.cuh", "fcirc_kernels.cuh", "matvec_impl.cuh", "apps.cuh", "plan.h", "runtime.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
@@ -43,8 +43,21 @@ def build(force: bool = False, verbose: bool = False, extra_flags=()) -> str:
         subprocess.check_call(cmd)
         return obj
 
-    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(compile_one, SOURCES))
+    hdr_t = max(os.path.getmtime(p) for p in [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "fcirc.h")]
+                if os.path.exists(p))
+
+    def obj_of(src):
+        return os.path.join(OBJ_DIR, src.rsplit(".", 1)[0] + ".o")
+
+    def stale_obj(src):   # object older than its source or any shared header (or extra flags given)
+        o = obj_of(src)
+        return force or extra_flags or not os.path.exists(o) or \
+            os.path.getmtime(o) < max(os.path.getmtime(os.path.join(CSRC, src)), hdr_t)
+
+    todo = [src for src in SOURCES if stale_obj(src)]
+    with cf.ThreadPoolExecutor(max_workers=max(1, len(todo))) as ex:
+        list(ex.map(compile_one, todo))
+    objs = [obj_of(src) for src in SOURCES]
     cmd = [nvcc, *ARCH, "-shared", *objs, "-o", LIB + ".tmp"]
     if verbose:
         print(" ".join(cmd), flush=True)

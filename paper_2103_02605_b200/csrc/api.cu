@@ -62,20 +62,48 @@ void prof_end(cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 void count_launch() { ++g_launches; }
 
+// Private per-device stream for plan uploads and stream-ordered table frees (non-blocking: never
+// synchronises with the legacy default stream or with callers' streams).
+static std::mutex g_priv_mu;
+static std::map<int, cudaStream_t> g_priv;
+static cudaStream_t plan_stream(int dev) {
+  std::lock_guard<std::mutex> lk(g_priv_mu);
+  auto it = g_priv.find(dev);
+  if (it != g_priv.end()) return it->second;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  g_priv[dev] = s;
+  return s;
+}
+
 DevPlan::~DevPlan() {
-  if (twf) cudaFree(twf);
-  if (twi) cudaFree(twi);
+  // Runs when the cache has dropped the plan and the last caller holding it has enqueued its work
+  // (and recorded its use event).  Frees stream-ordered after every recorded use: no device sync.
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  cudaStream_t ps = plan_stream(dev);
+  for (auto& u : uses) {
+    if (ps) cudaStreamWaitEvent(ps, u.second, 0);
+    cudaEventDestroy(u.second);   // released by the driver once the event has completed
+  }
+  if (twf) cudaFreeAsync(twf, ps);
+  if (twi) cudaFreeAsync(twi, ps);
+  if (cur != dev) cudaSetDevice(cur);
 }
 
 static std::mutex g_mu;
 static std::mutex g_host_mu;
 // plan cache keyed by (device, p, f, log2 n), least-recently-used eviction beyond kMaxPlans entries or
 // kMaxPlanBytes of device tables (callers with a new f per call would otherwise grow it without
-// bound); evicted tables are freed by the last shared_ptr owner (cudaFree synchronises the device).
+// bound).  Evicted tables are freed by DevPlan::~DevPlan after their recorded uses (stream-ordered).
+// A plan used while its stream is capturing a CUDA graph is pinned: never evicted (a graph may
+// replay it any time later); only fcirc_release_cache drops pinned plans.
 struct PlanEntry {
   std::shared_ptr<DevPlan> plan;
   uint64_t last_use = 0;
   size_t bytes = 0;
+  bool pinned = false;
 };
 static std::map<std::tuple<int, uint64_t, uint64_t, int>, PlanEntry> g_plans;
 static uint64_t g_plan_tick = 0;
@@ -84,13 +112,35 @@ static constexpr size_t kMaxPlans = 64;
 static constexpr size_t kMaxPlanBytes = (size_t)2 << 30;
 
 static void evict_plans_locked() {
-  while (g_plans.size() > kMaxPlans || (g_plan_bytes > kMaxPlanBytes && g_plans.size() > 1)) {
-    auto victim = g_plans.begin();
+  for (;;) {
+    size_t unpinned = 0;
+    for (auto& kv : g_plans) unpinned += !kv.second.pinned;
+    if (!(unpinned > 0 && (g_plans.size() > kMaxPlans || (g_plan_bytes > kMaxPlanBytes && g_plans.size() > 1))))
+      return;
+    auto victim = g_plans.end();
     for (auto it = g_plans.begin(); it != g_plans.end(); ++it)
-      if (it->second.last_use < victim->second.last_use) victim = it;
+      if (!it->second.pinned && (victim == g_plans.end() || it->second.last_use < victim->second.last_use)) victim = it;
+    if (victim == g_plans.end() || g_plans.size() - 1 < 1) return;
     g_plan_bytes -= victim->second.bytes;
     g_plans.erase(victim);
   }
+}
+
+// After a call enqueued work that reads the plan's tables on `st`: record (or re-record) the plan's
+// use event for `st`.  (Under capture get_plan has pinned the plan instead.)
+static void note_plan_use(DevPlan* dp, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaEvent_t ev = nullptr;
+  for (auto& u : dp->uses)
+    if (u.first == st) ev = u.second;
+  if (!ev) {
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return;
+    dp->uses.emplace_back(st, ev);
+  }
+  cudaEventRecord(ev, st);
 }
 
 static TwU32 shoup_pair(uint64_t w, uint64_t p) {
@@ -100,42 +150,59 @@ static TwU32 shoup_pair(uint64_t w, uint64_t p) {
   return t;
 }
 
-static int get_plan(int dev, uint64_t p, uint64_t f, int L, std::shared_ptr<DevPlan>* out) {
+// allocate + upload one table on the private stream (completion is awaited before publication)
+static int upload(void** dst, const void* src, size_t bytes, cudaStream_t ps) {
+  if (cudaMallocAsync(dst, bytes, ps) != cudaSuccess) return FCIRC_ENOMEM;
+  return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, ps) == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
+static int get_plan(int dev, uint64_t p, uint64_t f, int L, cudaStream_t st, std::shared_ptr<DevPlan>* out) {
   auto key = std::make_tuple(dev, p, f, L);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_plans.find(key);
     if (it != g_plans.end()) {
       it->second.last_use = ++g_plan_tick;
+      if (capturing) it->second.pinned = true;   // a captured graph may replay it at any later time
       *out = it->second.plan;
       return FCIRC_OK;
     }
   }
+  // a new plan needs host work, allocations and a synchronous upload: not inside a graph capture
+  if (capturing) return FCIRC_EINVAL;
   auto dp = std::make_shared<DevPlan>();
-  int st = build_host_plan(p, f, L, &dp->hp);
-  if (st != FCIRC_OK) return st;
+  dp->dev = dev;
+  int st_ = build_host_plan(p, f, L, &dp->hp);
+  if (st_ != FCIRC_OK) return st_;
+  cudaStream_t ps = plan_stream(dev);
+  if (!ps) return FCIRC_ECUDA;
   const PrimeInfo* pi = prime_info(p);
   const size_t n = dp->hp.s.size();
   size_t bytes = 0;
+  int rc = FCIRC_OK;
+  std::vector<TwU32> hf, hi;
   if (!pi->wide) {
-    std::vector<TwU32> hf(n), hi(n);
+    hf.resize(n);
+    hi.resize(n);
     for (size_t i = 0; i < n; ++i) { hf[i] = shoup_pair(dp->hp.s[i], p); hi[i] = shoup_pair(dp->hp.sinv[i], p); }
     bytes = 2 * n * sizeof(TwU32);
-    if (cudaMalloc(&dp->twf, n * sizeof(TwU32)) != cudaSuccess) return FCIRC_ENOMEM;
-    if (cudaMalloc(&dp->twi, n * sizeof(TwU32)) != cudaSuccess) return FCIRC_ENOMEM;
-    if (cudaMemcpy(dp->twf, hf.data(), n * sizeof(TwU32), cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
-    if (cudaMemcpy(dp->twi, hi.data(), n * sizeof(TwU32), cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
+    if (!rc) rc = upload(&dp->twf, hf.data(), n * sizeof(TwU32), ps);
+    if (!rc) rc = upload(&dp->twi, hi.data(), n * sizeof(TwU32), ps);
     dp->last_si32 = shoup_pair(dp->hp.last_si, p);
     dp->last_k32 = shoup_pair(dp->hp.K, p);
   } else {
     bytes = 2 * n * 8;
-    if (cudaMalloc(&dp->twf, n * 8) != cudaSuccess) return FCIRC_ENOMEM;
-    if (cudaMalloc(&dp->twi, n * 8) != cudaSuccess) return FCIRC_ENOMEM;
-    if (cudaMemcpy(dp->twf, dp->hp.s.data(), n * 8, cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
-    if (cudaMemcpy(dp->twi, dp->hp.sinv.data(), n * 8, cudaMemcpyHostToDevice) != cudaSuccess) return FCIRC_ECUDA;
+    if (!rc) rc = upload(&dp->twf, dp->hp.s.data(), n * 8, ps);
+    if (!rc) rc = upload(&dp->twi, dp->hp.sinv.data(), n * 8, ps);
     dp->last_si64 = dp->hp.last_si;
     dp->last_k64 = dp->hp.K;
   }
+  // the tables are complete on the device before any caller's stream can use the plan
+  if (cudaStreamSynchronize(ps) != cudaSuccess && !rc) rc = FCIRC_ECUDA;
+  if (rc) return rc;
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_plans.find(key);
   if (it != g_plans.end()) {  // another thread won
@@ -143,7 +210,7 @@ static int get_plan(int dev, uint64_t p, uint64_t f, int L, std::shared_ptr<DevP
     *out = it->second.plan;
     return FCIRC_OK;
   }
-  g_plans[key] = PlanEntry{dp, ++g_plan_tick, bytes};
+  g_plans[key] = PlanEntry{dp, ++g_plan_tick, bytes, false};
   g_plan_bytes += bytes;
   evict_plans_locked();
   *out = dp;
@@ -262,17 +329,19 @@ static int matvec_core(uint64_t p, uint64_t f, const void* a, const void* b, voi
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return FCIRC_ECUDA;
   std::shared_ptr<DevPlan> dp;
-  rc = get_plan(dev, p, f, L, &dp);
+  rc = get_plan(dev, p, f, L, st, &dp);
   if (rc) return rc;
   if (pi->kind == KIND_GOLD) {
     FieldGold fld;
-    return run_matvec_gold(fld, *dp, a, b, c, L, batch, st, dev, io);
-  }
-  if (pi->kind == KIND_M31X2) {
+    rc = run_matvec_gold(fld, *dp, a, b, c, L, batch, st, dev, io);
+  } else if (pi->kind == KIND_M31X2) {
     FieldM31x2 fld;
-    return run_matvec_m31(fld, *dp, a, b, c, L, batch, st, dev, io);
+    rc = run_matvec_m31(fld, *dp, a, b, c, L, batch, st, dev, io);
+  } else {
+    rc = run_matvec_u32(make_u32(p), *dp, a, b, c, L, batch, st, dev, io);
   }
-  return run_matvec_u32(make_u32(p), *dp, a, b, c, L, batch, st, dev, io);
+  note_plan_use(dp.get(), st);   // even after a failed launch: some kernels may be queued
+  return rc;
 }
 
 // fcirc_matvec without resetting the launch counter (also used by the host pipeline)
@@ -311,14 +380,38 @@ static int polymul_impl(uint64_t p, const void* a, int64_t na, const void* b, in
   return matvec_core(p, 1, a, b, c, ilog2_exact(next_pow2(io.nc)), batch, st, io);
 }
 
-// host buffers -> device -> host, pipelined over NSLOT streams (fcirc_matvec_host)
+// host buffers -> device -> host, pipelined over NSLOT streams (fcirc_matvec_host).  Each call takes
+// a context (streams + device staging buffers) from a per-device pool and returns it afterwards, so
+// concurrent host threads run their pipelines concurrently (one mutex only around take / return).
 struct HostCtx {
   static constexpr int NSLOT = 3;
+  int dev = 0;
   cudaStream_t st[NSLOT] = {};
   void* buf[NSLOT] = {};
   size_t bytes = 0;
 };
-static std::map<int, HostCtx> g_host;
+static std::vector<HostCtx*> g_host_free;   // idle contexts (any device), guarded by g_host_mu
+
+static HostCtx* host_ctx_take(int dev) {
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    for (size_t i = 0; i < g_host_free.size(); ++i)
+      if (g_host_free[i]->dev == dev) {
+        HostCtx* hc = g_host_free[i];
+        g_host_free.erase(g_host_free.begin() + i);
+        return hc;
+      }
+  }
+  HostCtx* hc = new HostCtx;
+  hc->dev = dev;
+  for (int i = 0; i < HostCtx::NSLOT; ++i)
+    if (cudaStreamCreateWithFlags(&hc->st[i], cudaStreamNonBlocking) != cudaSuccess) { delete hc; return nullptr; }
+  return hc;
+}
+static void host_ctx_return(HostCtx* hc) {
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  g_host_free.push_back(hc);
+}
 
 static int host_pipeline(uint64_t p, uint64_t f, const char* a, const char* b, char* c, int64_t n, int64_t batch,
                          size_t es, int dev) {
@@ -326,29 +419,27 @@ static int host_pipeline(uint64_t p, uint64_t f, const char* a, const char* b, c
   static const int64_t chunk_mb = std::max(1, knob("HOST_CHUNK_MB", 32));  // per operand and chunk
   const int64_t C = std::max<int64_t>(1, std::min<int64_t>(batch, (chunk_mb << 20) / (int64_t)inst_bytes));
   const size_t slot_bytes = 3 * (size_t)C * inst_bytes;
-  std::lock_guard<std::mutex> lk(g_host_mu);
-  HostCtx& hc = g_host[dev];
-  if (!hc.st[0])
-    for (int i = 0; i < HostCtx::NSLOT; ++i)
-      if (cudaStreamCreateWithFlags(&hc.st[i], cudaStreamNonBlocking) != cudaSuccess) return FCIRC_ECUDA;
-  if (hc.bytes < slot_bytes) {
+  HostCtx* hc = host_ctx_take(dev);
+  if (!hc) return FCIRC_ECUDA;
+  struct Ret { HostCtx* h; ~Ret() { host_ctx_return(h); } } ret{hc};
+  if (hc->bytes < slot_bytes) {
     for (int i = 0; i < HostCtx::NSLOT; ++i) {
-      cudaStreamSynchronize(hc.st[i]);
-      if (hc.buf[i]) cudaFree(hc.buf[i]);
-      hc.buf[i] = nullptr;
+      cudaStreamSynchronize(hc->st[i]);
+      if (hc->buf[i]) cudaFreeAsync(hc->buf[i], hc->st[i]);
+      hc->buf[i] = nullptr;
     }
-    hc.bytes = 0;
+    hc->bytes = 0;
     for (int i = 0; i < HostCtx::NSLOT; ++i)
-      if (cudaMalloc(&hc.buf[i], slot_bytes) != cudaSuccess) return FCIRC_ENOMEM;
-    hc.bytes = slot_bytes;
+      if (cudaMallocAsync(&hc->buf[i], slot_bytes, hc->st[i]) != cudaSuccess) return FCIRC_ENOMEM;
+    hc->bytes = slot_bytes;
   }
   int rc = FCIRC_OK;
   int64_t chunk = 0;
   for (int64_t i0 = 0; i0 < batch && rc == FCIRC_OK; i0 += C, ++chunk) {
     const int64_t cc = std::min<int64_t>(C, batch - i0);
     const int sl = (int)(chunk % HostCtx::NSLOT);
-    cudaStream_t st = hc.st[sl];
-    char* dA = (char*)hc.buf[sl];
+    cudaStream_t st = hc->st[sl];
+    char* dA = (char*)hc->buf[sl];
     char* dB = dA + (size_t)C * inst_bytes;
     char* dC = dB + (size_t)C * inst_bytes;
     const size_t off = (size_t)i0 * inst_bytes, nb = (size_t)cc * inst_bytes;
@@ -359,7 +450,7 @@ static int host_pipeline(uint64_t p, uint64_t f, const char* a, const char* b, c
     if (cudaMemcpyAsync(c + off, dC, nb, cudaMemcpyDeviceToHost, st) != cudaSuccess) rc = FCIRC_ECUDA;
   }
   for (int i = 0; i < HostCtx::NSLOT; ++i)
-    if (cudaStreamSynchronize(hc.st[i]) != cudaSuccess && rc == FCIRC_OK) rc = FCIRC_ECUDA;
+    if (cudaStreamSynchronize(hc->st[i]) != cudaSuccess && rc == FCIRC_OK) rc = FCIRC_ECUDA;
   return rc;
 }
 
@@ -572,15 +663,30 @@ int fcirc_profile_read(int64_t* counts, double* ms, int nkinds) {
 }
 
 int fcirc_release_cache(void) {
+  // drops every plan, pinned ones included: CUDA graphs captured over libfcirc calls must not be
+  // replayed afterwards (fcirc.h)
   cudaDeviceSynchronize();
-  std::lock_guard<std::mutex> lk(g_mu);
-  g_plans.clear();
-  g_plan_bytes = 0;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_plans.clear();
+    g_plan_bytes = 0;
+  }
   int dev = 0;
   cudaMemPool_t pool;
-  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
-    cudaMemPoolTrimTo(pool, 0);
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    cudaStream_t ps = plan_stream(dev);
+    if (ps) cudaStreamSynchronize(ps);
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
   return FCIRC_OK;
+}
+
+int64_t fcirc_plan_count(int* pinned) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int np = 0;
+  for (auto& kv : g_plans) np += kv.second.pinned;
+  if (pinned) *pinned = np;
+  return (int64_t)g_plans.size();
 }
 
 }  // extern "C"

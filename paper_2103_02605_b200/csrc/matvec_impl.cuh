@@ -78,11 +78,8 @@ static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t s
   constexpr int TGT = (RR <= 8 || (sizeof(E) == 4 && !TWS && !EMB && M == 12)) ? 1024 : 512;
   constexpr int MINB = (T * IPC < TGT) ? TGT / (T * IPC) : 1;
   auto kern = k_block<F, M, R, IPC, MINB, EMB, TWS>;
-  // opt-in shared memory, once per instantiation (thread-safe static initialisation)
-  static const bool attr_ok =
-      smem <= 48 * 1024 ||
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
-  if (!attr_ok) return FCIRC_ECUDA;
+  static std::atomic<uint32_t> attr_mask{0};   // opt-in shared memory once per (kernel, device)
+  if (!smem_optin((const void*)kern, smem, attr_mask)) return FCIRC_ECUDA;
   const int64_t batch = args.units >> args.k;
   BlockArgs<F> a2 = args;
   // staged sub-problem launches: each CTA walks seq instance groups of one sub-block, staging its
@@ -127,10 +124,8 @@ static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStr
   const size_t smem = (size_t)(1 << K) * W * sizeof(E);
   constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
   auto kern = k_cols<F, K, R, W, INV, MINB, EMB>;
-  static const bool attr_ok =
-      smem <= 48 * 1024 ||
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
-  if (!attr_ok) return FCIRC_ECUDA;
+  static std::atomic<uint32_t> attr_mask{0};   // opt-in shared memory once per (kernel, device)
+  if (!smem_optin((const void*)kern, smem, attr_mask)) return FCIRC_ECUDA;
   args.colblocks = args.m / W;
   args.units = instances * args.colblocks;
   dim3 grid((unsigned)args.units, INV ? 1 : 2);
@@ -153,10 +148,8 @@ static int launch_cols_fwd2(const F& fld, ColArgs<F> args, int64_t instances, cu
   constexpr int TGT = (RR <= 8 || sizeof(E) == 4) ? 1024 : 512;
   constexpr int MINB = (threads < TGT) ? TGT / threads : 1;
   auto kern = k_cols_fwd2<F, K, R, W, MINB, EMB>;
-  static const bool attr_ok =
-      smem <= 48 * 1024 ||
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
-  if (!attr_ok) return FCIRC_ECUDA;
+  static std::atomic<uint32_t> attr_mask{0};   // opt-in shared memory once per (kernel, device)
+  if (!smem_optin((const void*)kern, smem, attr_mask)) return FCIRC_ECUDA;
   args.colblocks = args.m / W;
   args.units = instances * args.colblocks;
   prof_begin(2, st);
@@ -175,10 +168,8 @@ static int launch_cols_inv2(const F& fld, ColArgs<F> args, int64_t instances, cu
   const size_t smem = (size_t)2 * (1 << K) * W * sizeof(E);
   constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
   auto kern = k_cols_inv2<F, K, R, W, MINB, EMB>;
-  static const bool attr_ok =
-      smem <= 48 * 1024 ||
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) == cudaSuccess;
-  if (!attr_ok) return FCIRC_ECUDA;
+  static std::atomic<uint32_t> attr_mask{0};   // opt-in shared memory once per (kernel, device)
+  if (!smem_optin((const void*)kern, smem, attr_mask)) return FCIRC_ECUDA;
   args.colblocks = args.m / (2 * W);
   args.units = instances * args.colblocks;
   prof_begin(3, st);
@@ -225,16 +216,11 @@ static int launch_cols_tma(const F& fld, ColArgs<F> args, int64_t instances, cud
   const size_t smem = (size_t)3 * (1 << K) * W * sizeof(E) + 16 + 128;
   constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
   auto kern = k_cols_tma<F, K, R, W, INV, MINB>;
-  // resident CTAs per SM, once per instantiation (thread-safe static initialisation; 0 = error)
-  static const int occ = [&] {
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return 0;
-    int o = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, threads, smem) != cudaSuccess) return 0;
-    return o;
-  }();
-  if (occ < 1) return FCIRC_ECUDA;
+  static std::atomic<uint32_t> attr_mask{0};   // opt-in shared memory once per (kernel, device)
+  if (!smem_optin((const void*)kern, smem, attr_mask)) return FCIRC_ECUDA;
+  int occ = 0;   // resident CTAs per SM (after the opt-in on this device)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1)
+    return FCIRC_ECUDA;
   args.colblocks = args.m / W;
   args.units = instances * args.colblocks;
   CUtensorMap m0, m1;
@@ -329,9 +315,12 @@ static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cud
       return launch_cols_inv2<F, K, 16>(fld, args, inst, st);
     }
   }
-  // TMA pipeline when two stages + the exchange buffer fit in shared memory
+  // TMA pipeline when two stages + the exchange buffer fit in shared memory and the tensor-map bases
+  // are 16-byte aligned (cuTensorMapEncodeTiled's requirement; an offset view of a caller's tensor
+  // may be only element-aligned and then takes the plain column kernels below)
   if constexpr (K >= FTraits<F>::TMA_MIN_K && 3 * (1 << K) * wsel<16>(K) * sizeof(E) <= 200 * 1024) {
-    if (use_tma) {
+    const bool aligned = ((uintptr_t)args.src0 & 15) == 0 && (INV || ((uintptr_t)args.src1 & 15) == 0);
+    if (use_tma && aligned) {
       if constexpr (K <= 10)
         if (r == 8) return launch_cols_tma<F, K, INV, 8>(fld, args, inst, st);
       return launch_cols_tma<F, K, INV, 16>(fld, args, inst, st);

@@ -4,8 +4,11 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <utility>
+#include <vector>
 
 #include "modarith.cuh"
 #include "plan.h"
@@ -13,14 +16,36 @@
 namespace fcirc {
 
 // A device-resident plan: the host tables of plan.h uploaded in the element layout of the field.
+// Lifetime (api.cu): the tables are allocated stream-ordered on a private per-device stream and
+// uploaded before the plan is published; every call that launches with the plan records an event
+// on its stream (`uses`, one event per stream), and the destructor -- run when the plan cache has
+// evicted the plan and the last caller holding it has finished enqueueing -- frees the tables with
+// cudaFreeAsync on the private stream after waiting on those events: no device-wide
+// synchronisation, no free before in-flight work is done.  Plans used inside a CUDA-graph capture
+// are pinned by the cache (never evicted) because a graph may replay them at any later time.
 struct DevPlan {
   HostPlan hp;
+  int dev = 0;
   void* twf = nullptr;  // TwU32[n] or uint64_t[n]: s_{d,e} at heap index 2^d + e
   void* twi = nullptr;  // s_{d,e}^-1
   TwU32 last_si32{}, last_k32{};
   uint64_t last_si64 = 0, last_k64 = 0;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;   // guarded by the plan-cache mutex
   ~DevPlan();
 };
+
+// Opt-in dynamic shared memory above 48 KB for `fn` on the CURRENT device, once per (kernel, device)
+// (kernel attributes are per device context): `mask` is one static per kernel instantiation.
+inline bool smem_optin(const void* fn, size_t smem, std::atomic<uint32_t>& mask) {
+  if (smem <= 48 * 1024) return true;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const uint32_t bit = 1u << (dev & 31);
+  if (mask.load(std::memory_order_acquire) & bit) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+  return true;
+}
 
 // launch bookkeeping (api.cu): optional per-launch CUDA-event timing and the launch counter
 void prof_begin(int kind, cudaStream_t st);

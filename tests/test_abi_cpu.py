@@ -260,3 +260,16 @@ def test_synth_edge_mix_is_canonical_and_hits_the_corners():
         for corner in (0, 1, p - 1, p - 2, (1 << 31) - 1):
             if corner < p:
                 assert (v == corner).any(), (p, corner)
+
+
+def test_primitive_rate_and_plan_count_validation_before_device():
+    """fcirc_primitive_rate rejects an unknown kind / non-positive iteration count before touching
+    the device; fcirc_plan_count is host-only."""
+    import ctypes
+    lib = fc._load()
+    ops = ctypes.c_double(0.0)
+    assert lib.fcirc_primitive_rate(99, 10, ctypes.byref(ops), None, None) == -1
+    assert lib.fcirc_primitive_rate(0, 0, ctypes.byref(ops), None, None) == -1
+    assert lib.fcirc_primitive_rate(0, 10, None, None, None) == -1
+    n, pinned = fc.plan_count()
+    assert n >= 0 and 0 <= pinned <= n
