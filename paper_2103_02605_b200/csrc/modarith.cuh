@@ -166,16 +166,21 @@ struct FieldGold {
   }
   // (t0 + t1 2^32 + t2 2^64 + t3 2^96) mod p, canonical, with 2^64 == EPS and 2^96 == -1:
   //   V = (t1:t0) + t2 EPS - t3 as a 3-word signed value c 2^64 + (r1:r0), c in {-1, 0, 1}
-  //       (V in (-2^32, 2^65 - 2^33]);
+  //       (V in (-2^32, 2^65 - 2^33]); (t1:t0) + t2 EPS is ONE IMAD.WIDE.U32 with carry out
+  //       (mul.wide.u32 + add.cc.u64; the former mad.lo.cc / madc.hi.cc pair compiled to
+  //       IMAD.IADD + IMAD.HI + a register-pair move: k_block -1.6 %, k_cols_inv2 -3.6 %,
+  //       profiles/r02a_gold_ab_reduce_variants.txt);
   //   r += c EPS  (as a 64-bit two's-complement add of (c >> 31 : -c)); for c = +1 the result is
   //       <= 2^64 - 2^32 - 1 < p, for c = -1 it is in [p - EPS, p), no further wrap;
   //   canonicalise: r >= p only if r_hi == 0xffffffff and r_lo != 0, and then r - p = (r_lo - 1, 0).
   __device__ __forceinline__ static uint64_t reduce4(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
     uint32_t r0, r1;
-    asm("{\n\t.reg .u32 c, m, h;\n\t.reg .pred p, q;\n\t"
-        "mad.lo.cc.u32   %0, %4, 0xffffffff, %2;\n\t"
-        "madc.hi.cc.u32  %1, %4, 0xffffffff, %3;\n\t"
+    asm("{\n\t.reg .u32 c, m, h;\n\t.reg .u64 T, E, R;\n\t.reg .pred p, q;\n\t"
+        "mov.b64         T, {%2, %3};\n\t"
+        "mul.wide.u32    E, %4, 0xffffffff;\n\t"
+        "add.cc.u64      R, T, E;\n\t"
         "addc.u32        c, 0, 0;\n\t"
+        "mov.b64         {%0, %1}, R;\n\t"
         "sub.cc.u32      %0, %0, %5;\n\t"
         "subc.cc.u32     %1, %1, 0;\n\t"
         "subc.u32        c, c, 0;\n\t"

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <random>
 #include <vector>
 
@@ -23,7 +24,7 @@ template <int V>
 struct GV : FieldGold {
   // reduce variants
   __device__ __forceinline__ static uint64_t red(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
-    if constexpr (V == 0) {
+    if constexpr (V == 0 || V == 4) {
       return reduce4(t0, t1, t2, t3);
     } else if constexpr (V == 2) {
       uint32_t r0, r1;
@@ -75,7 +76,33 @@ struct GV : FieldGold {
       return mk(r0, r1);
     }
   }
+  // V >= 3: the 64 x 64 product as four mul.wide.u32 partials with explicit carry chains (ptxas then
+  // emits 4 IMAD.WIDE.U32 + 4 carry instructions; the C-level lo/hi form sometimes recomputes a0 b0)
+  __device__ __forceinline__ static void prod(uint64_t a, uint64_t b, uint32_t& t0, uint32_t& t1, uint32_t& t2,
+                                              uint32_t& t3) {
+    asm("{\n\t.reg .u32 a0, a1, b0, b1, l1, c0, c1, h0, h1, k;\n\t.reg .u64 L, X, Y, H;\n\t"
+        "mov.b64 {a0, a1}, %4;\n\t"
+        "mov.b64 {b0, b1}, %5;\n\t"
+        "mul.wide.u32 L, a0, b0;\n\t"
+        "mul.wide.u32 X, a0, b1;\n\t"
+        "mul.wide.u32 Y, a1, b0;\n\t"
+        "add.cc.u64 X, X, Y;\n\t"
+        "addc.u32 k, 0, 0;\n\t"
+        "mul.wide.u32 H, a1, b1;\n\t"
+        "mov.b64 {%0, l1}, L;\n\t"
+        "mov.b64 {c0, c1}, X;\n\t"
+        "mov.b64 {h0, h1}, H;\n\t"
+        "add.cc.u32 %1, l1, c0;\n\t"
+        "addc.cc.u32 %2, h0, c1;\n\t"
+        "addc.u32 %3, h1, k;\n\t}"
+        : "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3) : "l"(a), "l"(b));
+  }
   __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
+    if constexpr (V >= 3) {
+      uint32_t t0, t1, t2, t3;
+      prod(a, b, t0, t1, t2, t3);
+      return red(t0, t1, t2, t3);
+    }
     const uint64_t lo = a * b, hi = __umul64hi(a, b);
     return red(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
   }
@@ -197,9 +224,10 @@ int main(int argc, char** argv) {
   // opt-in smem for the fwd/inv kernels (32 KB: not needed) -- k_block needs 64 KB
   std::vector<uint64_t> rb, rf, ri;
   for (int round = 0; round < 2; ++round) {   // two rounds: A B A B
-    bench<0>("current", reps, B, &rb, &rf, &ri);
+    bench<0>("round-1 reduce", reps, B, &rb, &rf, &ri);
     bench<1>("wide-eps reduce", reps, B, &rb, &rf, &ri);
-    bench<2>("wide-eps reduce, carry-select canonicalisation", reps, B, &rb, &rf, &ri);
+    bench<3>("explicit mul.wide product + wide-eps reduce", reps, B, &rb, &rf, &ri);
+    bench<4>("explicit mul.wide product + round-1 reduce", reps, B, &rb, &rf, &ri);
   }
   return 0;
 }

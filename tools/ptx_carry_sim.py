@@ -11,6 +11,8 @@ becomes `IMAD.X m, RZ, RZ, -1, P` = carry - 1):
                                 subc:    d = a + ~b + CF
                                 mad.lo.cc / madc.hi.cc: lo/hi 32 bits of a*b, plus c (+ CF)
     setp.{eq,ne}[.and].u32 and @p / @!p predication: plain predicate semantics
+    64-bit registers:           mov.b64 D, {lo, hi} / mov.b64 {lo, hi}, D;  mul.wide.u32 D, a, b;
+                                add.cc.u64 D, A, B (CF = carry out of 2^64)
 
 so a helper can be checked exhaustively on edge values and randomly against Python integers
 without a GPU.  Used by tests/test_modarith_ptx.py.
@@ -67,8 +69,25 @@ def run(text: str, nout: int, inputs):
             if pv == neg:
                 continue
             op, rest = rest.split(None, 1)
+        if op == "mov.b64":             # pack / unpack a 64-bit register (braces hold a register pair)
+            m = re.match(r"\{\s*(\S+)\s*,\s*(\S+)\s*\}\s*,\s*(\S+)$", rest.strip())
+            if m:                        # mov.b64 {lo, hi}, D
+                v = regs[m.group(3)]
+                regs[m.group(1)], regs[m.group(2)] = v & M32, v >> 32
+                continue
+            m = re.match(r"(\S+)\s*,\s*\{\s*(\S+)\s*,\s*(\S+)\s*\}$", rest.strip())
+            regs[m.group(1)] = val(m.group(2)) | (val(m.group(3)) << 32)
+            continue
         args = [a.strip() for a in rest.split(",")]
         d = args[0]
+        if op == "mul.wide.u32":
+            regs[d] = val(args[1]) * val(args[2])
+            continue
+        if op == "add.cc.u64":
+            r = regs[args[1]] + regs[args[2]]
+            cf = r >> 64
+            regs[d] = r & ((1 << 64) - 1)
+            continue
         if op.startswith("setp."):       # setp.{eq,ne}[.and].u32 p, a, b[, q]
             parts = op.split(".")
             cmp = parts[1]
