@@ -15,7 +15,7 @@ LIB_DIR = os.path.join(HERE, "lib")
 OBJ_DIR = os.path.join(LIB_DIR, "obj")
 LIB = os.path.join(LIB_DIR, "libfcirc.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-SOURCES = ["matvec_gold.cu", "matvec_u32.cu", "matvec_m31.cu", "api.cu", "plan.cpp", "probe.cu"]
+SOURCES = ["matvec_gold.cu", "matvec_u32.cu", "matvec_u32m.cu", "matvec_m31.cu", "api.cu", "plan.cpp", "probe.cu"]
 HEADERS = ["modarith.cuh", "fcirc_kernels.cuh", "matvec_impl.cuh", "apps.cuh", "plan.h", "runtime.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]

@@ -474,15 +474,35 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   uint32_t* r3 = r2 + batch * L;
   uint32_t* E = r3 + batch * L;
   uint32_t* S = E + batch * nd;
-  // 16-bit limb split + a~ embedding fused into the first pass of each product (EMB_LIMBS)
+  // 16-bit limb split + a~ embedding fused into the first pass (EMB_LIMBS); the three primes' f = 1
+  // products run as ONE product of 3 batch instances per pass (instance q batch + i = prime q,
+  // operands of instance i), outputs r1 | r2 | r3 contiguous.  FCIRC_BIGINT_SPLIT=1
+  // issues the three products separately (A/B).
   EmbedIO io;
   io.mode = EMB_LIMBS;
   io.na = nx;
   io.nb = ny;
   const int lg = ilog2_exact(L);
-  if ((rc = matvec_core(P1, 1, x, y, r1, lg, batch, st, io))) return rc;
-  if ((rc = matvec_core(P2, 1, x, y, r2, lg, batch, st, io))) return rc;
-  if ((rc = matvec_core(P3, 1, x, y, r3, lg, batch, st, io))) return rc;
+  static const int split = knob("BIGINT_SPLIT", 0);
+  if (split) {
+    if ((rc = matvec_core(P1, 1, x, y, r1, lg, batch, st, io))) return rc;
+    if ((rc = matvec_core(P2, 1, x, y, r2, lg, batch, st, io))) return rc;
+    if ((rc = matvec_core(P3, 1, x, y, r3, lg, batch, st, io))) return rc;
+  } else {
+    const uint64_t ps[3] = {P1, P2, P3};
+    std::shared_ptr<DevPlan> dp[3];
+    MultiPrime mp;
+    mp.n = 3;
+    mp.per = batch;
+    for (int q = 0; q < 3; ++q) {
+      if ((rc = get_plan(dev, ps[q], 1, lg, st, &dp[q]))) return rc;
+      mp.ps[q] = PrimeSel{make_u32(ps[q]), (const TwU32*)dp[q]->twf, (const TwU32*)dp[q]->twi, dp[q]->last_si32,
+                          dp[q]->last_k32};
+    }
+    rc = run_matvec_u32m(*dp[0], x, y, r1, lg, 3 * batch, st, dev, io, mp);
+    for (int q = 0; q < 3; ++q) note_plan_use(dp[q].get(), st);
+    if (rc) return rc;
+  }
   GarnerConsts g;
   g.p1 = (uint32_t)P1; g.p2 = (uint32_t)P2; g.p3 = (uint32_t)P3;
   g.p1p2 = P1 * P2;

@@ -22,6 +22,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "modarith.cuh"
 
@@ -121,6 +122,72 @@ __device__ __forceinline__ void io_store(T* dst, int64_t inst, int64_t pos, int6
   } else {
     dst[inst * n + pos] = v;
   }
+}
+
+// ------------------------------------------------------------------------------------------
+// Several 32-bit primes in ONE launch (bigint_mul's three CRT products):
+// instance j of the launch belongs to prime q = (inst0 + j) / per and reads the operands of instance
+// (inst0 + j) % per; each prime brings its field constants and twist tables.  A CTA that stages
+// twiddles in shared memory serves one prime only (the launcher keeps its instance groups inside
+// one prime); unstaged kernels select per thread.
+// ------------------------------------------------------------------------------------------
+struct PrimeSel {
+  FieldU32 fld;
+  const TwU32* twf;
+  const TwU32* twi;
+  TwU32 last_si, last_k;
+};
+struct MultiPrime {
+  int n = 1;             // primes in the launch (the FieldU32M kernels read it; others ignore it)
+  int64_t per = 1;       // instances per prime
+  int64_t inst0 = 0;     // global instance index of the launch's instance 0 (multi-pass chunks)
+  PrimeSel ps[3];
+};
+// the field constants and tables an instance uses
+template <class F>
+struct FieldView {
+  F fld;
+  const typename F::Tw* twf;
+  const typename F::Tw* twi;
+  typename F::Tw last_si, last_k;
+};
+// The multi-prime kernels are the FieldU32M instantiations, a distinct field type, so that the
+// single-field kernels carry neither the prime table in their parameters nor the selection code:
+// both measurably changed ptxas's output for the register-tight u32 column passes (a run-time
+// branch: C3 -18 %; a larger parameter block or local copies of the parameters: +8..25 % SASS in
+// the embedded u32 column passes, C3 -9 %; profiles/r02c_ab*.txt).
+struct FieldU32M : FieldU32 {};
+template <class F>
+constexpr bool kMulti = std::is_same<F, FieldU32M>::value;
+
+// Single-field kernels get an empty view and keep reading the kernel parameters at their uses.
+struct NoView {};
+template <class F, class A>
+__device__ __forceinline__ auto field_view(const F& fld, const A& args, int64_t inst) {
+  if constexpr (kMulti<F>) {
+    const int64_t q = (args.mp.inst0 + inst) / args.mp.per;
+    const PrimeSel& ps = q == 0 ? args.mp.ps[0] : (q == 1 ? args.mp.ps[1] : args.mp.ps[2]);
+    return FieldView<F>{F{ps.fld}, ps.twf, ps.twi, ps.last_si, ps.last_k};
+  } else {
+    (void)fld; (void)args; (void)inst;
+    return NoView{};
+  }
+}
+template <class F> __device__ __forceinline__ const F& select_field(const FieldView<F>& v, const F&) { return v.fld; }
+template <class F> __device__ __forceinline__ const F& select_field(const NoView&, const F& param) { return param; }
+template <class F, class A> __device__ __forceinline__ const typename F::Tw* view_twf(const FieldView<F>& v, const A&) { return v.twf; }
+template <class F, class A> __device__ __forceinline__ const typename F::Tw* view_twf(const NoView&, const A& a) { return a.twf; }
+template <class F, class A> __device__ __forceinline__ const typename F::Tw* view_twi(const FieldView<F>& v, const A&) { return v.twi; }
+template <class F, class A> __device__ __forceinline__ const typename F::Tw* view_twi(const NoView&, const A& a) { return a.twi; }
+template <class F, class A> __device__ __forceinline__ typename F::Tw view_lsi(const FieldView<F>& v, const A&) { return v.last_si; }
+template <class F, class A> __device__ __forceinline__ typename F::Tw view_lsi(const NoView&, const A& a) { return a.last_si; }
+template <class F, class A> __device__ __forceinline__ typename F::Tw view_lk(const FieldView<F>& v, const A&) { return v.last_k; }
+template <class F, class A> __device__ __forceinline__ typename F::Tw view_lk(const NoView&, const A& a) { return a.last_k; }
+// the caller's instance whose operands instance `inst` of the launch reads
+template <class F, class A>
+__device__ __forceinline__ int64_t src_inst(const A& args, int64_t inst) {
+  if constexpr (kMulti<F>) return (args.mp.inst0 + inst) % args.mp.per;
+  else return inst;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -235,6 +302,9 @@ struct BlockArgs {
   EmbedIO io;               // k == 0 and EMB only: embedding of the loads / truncation of the stores
   int seq = 1;              // instance groups per CTA, one after another (sharing staged twiddles)
 };
+// kernel argument type (see ColKArgs below): the multi-prime instantiations add the prime table
+template <class F> struct BlockArgsM : BlockArgs<F> { MultiPrime mp; };
+template <class F> using BlockKArgs = typename std::conditional<kMulti<F>, BlockArgsM<F>, BlockArgs<F>>::type;
 
 // k_block stages its twiddle slices in shared memory for the 32-bit fields (see TWS below), at
 // swizzled positions i ^ ((i >> 4) & 31) (a bijection of [0, 2^M)): the model in
@@ -242,10 +312,11 @@ struct BlockArgs {
 __device__ __forceinline__ int tw_swz(int i) { return i ^ ((i >> 4) & 31); }
 template <class F, int M> struct TwStage { static constexpr bool value = false; };
 template <int M> struct TwStage<FieldU32, M> { static constexpr bool value = M >= 6; };
+template <int M> struct TwStage<FieldU32M, M> { static constexpr bool value = M >= 6; };
 
 template <class F, int M, int R, int IPC, int MINB = 1, bool EMB = false, bool TWS = false>
 __global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
-k_block(F fld, BlockArgs<F> args) {
+k_block(F fld0, BlockKArgs<F> args) {
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<M, R>;
@@ -264,6 +335,11 @@ k_block(F fld, BlockArgs<F> args) {
 
   const int k = args.k;
   const int64_t batch = args.units >> k;
+  const int nseq = TWS ? args.seq : 1;   // unstaged launches: one group (no loop, no extra registers)
+  // field and tables: per CTA when staged (the launcher keeps a staged CTA inside one prime), else
+  // per instance group (the only group of the thread)
+  const auto fv = field_view(fld0, args, ((int64_t)(blockIdx.x >> k) * nseq) * IPC + (TWS ? 0 : li));
+  const F& fld = select_field(fv, fld0);
 
   // Twiddle staging (32-bit fields): sub-block E uses the heap slice
   // {2^(k+j) + E 2^j + e' : j < M, e' < 2^j} of each table (contiguous per level).
@@ -277,8 +353,8 @@ k_block(F fld, BlockArgs<F> args) {
     for (int h = threadIdx.x + 1; h < m; h += blockDim.x) {
       const int j = 31 - __clz(h);
       const int g = (1 << (k + j)) + (E << j) + (h - (1 << j));
-      twsf[tw_swz(h)] = args.twf[g];
-      twsi[tw_swz(h)] = args.twi[g];
+      twsf[tw_swz(h)] = view_twf<F>(fv, args)[g];
+      twsi[tw_swz(h)] = view_twi<F>(fv, args)[g];
     }
   };
   int gbase = 0;   // heap-extended address base of the current sub-block (fits: < 2n <= 2^24)
@@ -303,7 +379,6 @@ k_block(F fld, BlockArgs<F> args) {
     stage(E);
     __syncthreads();
   }
-  const int nseq = TWS ? args.seq : 1;   // unstaged launches: one group (no loop, no extra registers)
   for (int it = 0; it < nseq; ++it) {
   const int64_t inst = ((int64_t)(blockIdx.x >> k) * nseq + it) * IPC + li;
   const bool active = inst < batch;
@@ -316,8 +391,8 @@ k_block(F fld, BlockArgs<F> args) {
     for (int s = 0; s < R; ++s) {
       const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
       if constexpr (EMB) {
-        xa[s] = io_load(args.a, inst, ad, m, false, args.io);
-        xb[s] = io_load(args.b, inst, ad, m, true, args.io);
+        xa[s] = io_load(args.a, src_inst<F>(args, inst), ad, m, false, args.io);
+        xb[s] = io_load(args.b, src_inst<F>(args, inst), ad, m, true, args.io);
       } else {
         xa[s] = args.a[base + ad];
         xb[s] = args.b[base + ad];
@@ -333,7 +408,7 @@ k_block(F fld, BlockArgs<F> args) {
   for (int ph = 0; ph < NPH; ++ph) {
     if (ph > 0) exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx);
     forward_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
-      const Tw tw = tw_at(args.twf, twsf, bit, tb, cs);
+      const Tw tw = tw_at(view_twf<F>(fv, args), twsf, bit, tb, cs);
       fld.fwd_a(xa[s0], xa[s1], tw);
       fld.fwd_b(xb[s0], xb[s1], tw);
     });
@@ -342,7 +417,7 @@ k_block(F fld, BlockArgs<F> args) {
   // ---- leaves: 1x1 products (the recursion bottom), same thread/slot layout
   if constexpr (M == 0) {
     if (active) {
-      const T v = fld.single(xa[0], xb[0], args.last_k);
+      const T v = fld.single(xa[0], xb[0], view_lk<F>(fv, args));
       if constexpr (EMB) io_store(args.out, inst, 0, 1, v, args.io);
       else args.out[base] = v;
     }
@@ -357,8 +432,8 @@ k_block(F fld, BlockArgs<F> args) {
     for (int ph = NPH - 1; ph >= 0; --ph) {
       if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx);
       inverse_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
-        if (bit == M - 1 && top) fld.inv_last(xm[s0], xm[s1], args.last_si, args.last_k);
-        else fld.inv(xm[s0], xm[s1], tw_at(args.twi, twsi, bit, tb, cs));
+        if (bit == M - 1 && top) fld.inv_last(xm[s0], xm[s1], view_lsi<F>(fv, args), view_lk<F>(fv, args));
+        else fld.inv(xm[s0], xm[s1], tw_at(view_twi<F>(fv, args), twsi, bit, tb, cs));
       });
     }
 
@@ -394,6 +469,11 @@ struct ColArgs {
   typename F::Tw last_k;
   EmbedIO io;                 // EMB only: forward embedding of the loads; inverse truncation of the stores
 };
+
+// Kernel argument types: the FieldU32M (multi-prime) instantiations take the argument struct plus
+// the prime table; every other field takes the plain struct (unchanged parameter block).
+template <class F> struct ColArgsM : ColArgs<F> { MultiPrime mp; };
+template <class F> using ColKArgs = typename std::conditional<kMulti<F>, ColArgsM<F>, ColArgs<F>>::type;
 
 // row swizzle (GF(2)-linear bijection of [0, 2^K)): with the short phase on top, the rows a warp
 // touches in one access land in distinct banks in every phase (tools/bank_model.py)
@@ -439,7 +519,7 @@ __device__ __forceinline__ void col_inverse(T (&x)[R], T (*y)[R], T* bx, T* by, 
 // k_cols: one operand per thread; the forward pass covers a (blockIdx.y = 0) and b (= 1)
 template <class F, int K, int R, int W, bool INV, int MINB = 1, bool EMB = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
-k_cols(F fld, ColArgs<F> args) {
+k_cols(F fld0, ColKArgs<F> args) {
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<K, R>;
@@ -457,25 +537,27 @@ k_cols(F fld, ColArgs<F> args) {
   const T* src = second ? args.src1 : args.src0;
   T* dst = second ? args.dst1 : args.dst0;
   const ColIdx<PH, W> idx{c};
+  const auto fv = field_view(fld0, args, inst);
+  const F& fld = select_field(fv, fld0);
 
   T x[R];
   const int ph_in = INV ? NPH - 1 : 0, ph_out = INV ? 0 : NPH - 1;
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     const int64_t row = PH::ins_t(ph_in, t) + PH::cslot(ph_in, s);
-    if constexpr (EMB && !INV) x[s] = io_load(src, inst, col + row * m, args.n, second, args.io);
+    if constexpr (EMB && !INV) x[s] = io_load(src, src_inst<F>(args, inst), col + row * m, args.n, second, args.io);
     else x[s] = src[base + row * m];
   }
   if constexpr (!INV) {
     col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
-      const Tw tw = col_tw<K>(args.twf, bit, tb, cs);
+      const Tw tw = col_tw<K>(view_twf<F>(fv, args), bit, tb, cs);
       if (second) fld.fwd_b(x[s0], x[s1], tw);
       else fld.fwd_a(x[s0], x[s1], tw);
     });
   } else {
     col_inverse<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
-      if (bit == K - 1) fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
-      else fld.inv(x[s0], x[s1], col_tw<K>(args.twi, bit, tb, cs));
+      if (bit == K - 1) fld.inv_last(x[s0], x[s1], view_lsi<F>(fv, args), view_lk<F>(fv, args));
+      else fld.inv(x[s0], x[s1], col_tw<K>(view_twi<F>(fv, args), bit, tb, cs));
     });
   }
 #pragma unroll
@@ -494,7 +576,7 @@ k_cols(F fld, ColArgs<F> args) {
 // ------------------------------------------------------------------------------------------
 template <class F, int K, int R, int W, int MINB = 1, bool EMB = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
-k_cols_fwd2(F fld, ColArgs<F> args) {
+k_cols_fwd2(F fld0, ColKArgs<F> args) {
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<K, R>;
@@ -510,6 +592,8 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
   const int64_t base = inst * args.n + col;
   const int64_t m = args.m;
   const ColIdx<PH, W> idx{c};
+  const auto fv = field_view(fld0, args, inst);
+  const F& fld = select_field(fv, fld0);
 
   constexpr bool OFF32 = sizeof(T) == 8;   // 32-bit row offsets (row m < n <= 2^24) from opaque bases
   const uint32_t mm = (uint32_t)m;
@@ -520,8 +604,8 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
   for (int s = 0; s < R; ++s) {
     const int64_t row = PH::ins_t(0, t) + PH::cslot(0, s);
     if constexpr (EMB) {
-      xa[s] = io_load(args.src0, inst, col + row * m, args.n, false, args.io);
-      xb[s] = io_load(args.src1, inst, col + row * m, args.n, true, args.io);
+      xa[s] = io_load(args.src0, src_inst<F>(args, inst), col + row * m, args.n, false, args.io);
+      xb[s] = io_load(args.src1, src_inst<F>(args, inst), col + row * m, args.n, true, args.io);
     } else if constexpr (OFF32) {
       xa[s] = pa[(uint32_t)row * mm];
       xb[s] = pb[(uint32_t)row * mm];
@@ -531,7 +615,7 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
     }
   }
   col_forward<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
-    const Tw tw = col_tw<K>(args.twf, bit, tb, cs);
+    const Tw tw = col_tw<K>(view_twf<F>(fv, args), bit, tb, cs);
     fld.fwd_a(xa[s0], xa[s1], tw);
     fld.fwd_b(xb[s0], xb[s1], tw);
   });
@@ -557,7 +641,7 @@ k_cols_fwd2(F fld, ColArgs<F> args) {
 // ------------------------------------------------------------------------------------------
 template <class F, int K, int R, int W, int MINB = 1, bool EMB = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
-k_cols_inv2(F fld, ColArgs<F> args) {
+k_cols_inv2(F fld0, ColKArgs<F> args) {
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<K, R>;
@@ -572,6 +656,8 @@ k_cols_inv2(F fld, ColArgs<F> args) {
   const int64_t base = inst * args.n + (blockIdx.x - inst * args.colblocks) * 2 * W + c;
   const int64_t m = args.m;
   const ColIdx<PH, W> idx{c};
+  const auto fv = field_view(fld0, args, inst);
+  const F& fld = select_field(fv, fld0);
 
   T xa[R], xb[R];
 #pragma unroll
@@ -582,10 +668,10 @@ k_cols_inv2(F fld, ColArgs<F> args) {
   }
   col_inverse<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
     if (bit == K - 1) {
-      fld.inv_last(xa[s0], xa[s1], args.last_si, args.last_k);
-      fld.inv_last(xb[s0], xb[s1], args.last_si, args.last_k);
+      fld.inv_last(xa[s0], xa[s1], view_lsi<F>(fv, args), view_lk<F>(fv, args));
+      fld.inv_last(xb[s0], xb[s1], view_lsi<F>(fv, args), view_lk<F>(fv, args));
     } else {
-      const Tw tw = col_tw<K>(args.twi, bit, tb, cs);
+      const Tw tw = col_tw<K>(view_twi<F>(fv, args), bit, tb, cs);
       fld.inv(xa[s0], xa[s1], tw);
       fld.inv(xb[s0], xb[s1], tw);
     }
@@ -647,7 +733,7 @@ constexpr int kTmaBoxRows = 256;   // TMA box extent limit per dimension
 
 template <class F, int K, int R, int W, bool INV, int MINB = 1>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
-k_cols_tma(F fld, ColArgs<F> args, const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
+k_cols_tma(F fld0, ColKArgs<F> args, const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
            int64_t ntiles) {
   using T = typename F::T;
   using Tw = typename F::Tw;
@@ -707,6 +793,8 @@ k_cols_tma(F fld, ColArgs<F> args, const __grid_constant__ CUtensorMap map0, con
     decode(tile, inst, cb, second);
     const int64_t base = inst * args.n + cb * W + c;
     T* dst = second ? args.dst1 : args.dst0;
+    const auto fv = field_view(fld0, args, inst);
+    const F& fld = select_field(fv, fld0);
     mbar_wait(&bars[st], (uint32_t)((it >> 1) & 1));
     const T* tb_s = stage_buf + (size_t)st * ROWS * W;
 
@@ -716,14 +804,14 @@ k_cols_tma(F fld, ColArgs<F> args, const __grid_constant__ CUtensorMap map0, con
     for (int s = 0; s < R; ++s) x[s] = tb_s[(PH::ins_t(ph_in, t) + PH::cslot(ph_in, s)) * W + c];
     if constexpr (!INV) {
       col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
-        const Tw tw = col_tw<K>(args.twf, bit, tb, cs);
+        const Tw tw = col_tw<K>(view_twf<F>(fv, args), bit, tb, cs);
         if (second) fld.fwd_b(x[s0], x[s1], tw);
         else fld.fwd_a(x[s0], x[s1], tw);
       });
     } else {
       col_inverse<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
-        if (bit == K - 1) fld.inv_last(x[s0], x[s1], args.last_si, args.last_k);
-        else fld.inv(x[s0], x[s1], col_tw<K>(args.twi, bit, tb, cs));
+        if (bit == K - 1) fld.inv_last(x[s0], x[s1], view_lsi<F>(fv, args), view_lk<F>(fv, args));
+        else fld.inv(x[s0], x[s1], col_tw<K>(view_twi<F>(fv, args), bit, tb, cs));
       });
     }
 #pragma unroll

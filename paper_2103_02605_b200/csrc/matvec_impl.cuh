@@ -31,6 +31,7 @@ template <> struct FTraits<FieldU32> {
   static constexpr int TMA_MIN_K = 9;   // TMA inverse column passes from this depth on; below it
                                         // k_cols_inv2 measured faster (profiles/r01e_sweep_inv2.txt)
 };
+template <> struct FTraits<FieldU32M> : FTraits<FieldU32> {};   // multi-prime launches (bigint)
 template <> struct FTraits<FieldGold> {
   static constexpr int MMAX = 13;   // 2 x 2^13 x 8 B = 128 KB smem per sub-problem
   static constexpr int MPREF = 12;  // 64 KB: two CTAs per SM
@@ -64,7 +65,7 @@ template <int RR> constexpr int wsel(int K) {
 }
 
 template <class F, int M, int RR, bool EMB, bool TWS>
-static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
+static int launch_block_t(const F& fld, const BlockKArgs<F>& args, cudaStream_t st) {
   constexpr int R = rsel<RR>(M), IPC = ipcsel<RR>(M);
   constexpr int T = (1 << M) / R;
   using E = typename F::T;
@@ -81,7 +82,7 @@ static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t s
   static std::atomic<uint32_t> attr_mask{0};   // opt-in shared memory once per (kernel, device)
   if (!smem_optin((const void*)kern, smem, attr_mask)) return FCIRC_ECUDA;
   const int64_t batch = args.units >> args.k;
-  BlockArgs<F> a2 = args;
+  BlockKArgs<F> a2 = args;
   // staged sub-problem launches: each CTA walks seq instance groups of one sub-block, staging its
   // twiddle slice once (FCIRC_<field>_SEQ; default: the largest power of two <= 16 that still
   // leaves >= 1024 CTAs, about 3.5 waves of resident CTAs -- measured best for S1 (16), C3 (8)
@@ -96,6 +97,10 @@ static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t s
         while (seq < 16 && ((groups / (2 * seq)) << args.k) >= 1024) seq *= 2;
     }
     a2.seq = (int)std::min<int64_t>(seq, groups);
+    // several primes in one launch: a staged CTA's instances must stay inside one prime
+    if constexpr (kMulti<F>)
+      while (a2.seq > 1 && ((args.mp.per % ((int64_t)IPC * a2.seq)) != 0 || (args.mp.inst0 % ((int64_t)IPC * a2.seq)) != 0))
+        a2.seq >>= 1;
   }
   const int64_t per_cta = (int64_t)IPC * a2.seq;
   const int64_t grid = ((batch + per_cta - 1) / per_cta) << args.k;
@@ -110,14 +115,19 @@ static int launch_block_t(const F& fld, const BlockArgs<F>& args, cudaStream_t s
 // fused launches of a small batch (latency-bound: one coalesced table load per CTA instead of a
 // dependent L2 round trip per phase); large fused batches share the table through L1/L2 instead.
 template <class F, int M, int RR, bool EMB = false>
-static int launch_block(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
-  if constexpr (TwStage<F, M>::value && !EMB)
-    if (args.k > 0 || args.units <= 64) return launch_block_t<F, M, RR, false, true>(fld, args, st);
+static int launch_block(const F& fld, const BlockKArgs<F>& args, cudaStream_t st) {
+  if constexpr (TwStage<F, M>::value && !EMB) {
+    bool one_prime_per_cta = true;   // multi-prime: a staged CTA's IPC instances inside one prime
+    if constexpr (kMulti<F>)
+      one_prime_per_cta = args.mp.per % ipcsel<RR>(M) == 0 && args.mp.inst0 % ipcsel<RR>(M) == 0;
+    if ((args.k > 0 || args.units <= 64) && one_prime_per_cta)
+      return launch_block_t<F, M, RR, false, true>(fld, args, st);
+  }
   return launch_block_t<F, M, RR, EMB, false>(fld, args, st);
 }
 
 template <class F, int K, bool INV, int RR, bool EMB = false>
-static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
+static int launch_cols(const F& fld, ColKArgs<F> args, int64_t instances, cudaStream_t st) {
   constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
   constexpr int threads = W * ((1 << K) / R);
   using E = typename F::T;
@@ -138,7 +148,7 @@ static int launch_cols(const F& fld, ColArgs<F> args, int64_t instances, cudaStr
 
 // dual forward column pass (a and b per thread)
 template <class F, int K, int RR, bool EMB = false>
-static int launch_cols_fwd2(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
+static int launch_cols_fwd2(const F& fld, ColKArgs<F> args, int64_t instances, cudaStream_t st) {
   constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
   constexpr int threads = W * ((1 << K) / R);
   using E = typename F::T;
@@ -161,7 +171,7 @@ static int launch_cols_fwd2(const F& fld, ColArgs<F> args, int64_t instances, cu
 
 // inverse column pass, two column groups per thread (plain operands; needs m >= 2 W)
 template <class F, int K, int RR, bool EMB = false>
-static int launch_cols_inv2(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
+static int launch_cols_inv2(const F& fld, ColKArgs<F> args, int64_t instances, cudaStream_t st) {
   constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
   constexpr int threads = W * ((1 << K) / R);
   using E = typename F::T;
@@ -208,7 +218,7 @@ static bool make_col_map(CUtensorMap* map, const void* base, int64_t m, int K, i
 }
 
 template <class F, int K, bool INV, int RR>
-static int launch_cols_tma(const F& fld, ColArgs<F> args, int64_t instances, cudaStream_t st) {
+static int launch_cols_tma(const F& fld, ColKArgs<F> args, int64_t instances, cudaStream_t st) {
   constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
   constexpr int threads = W * ((1 << K) / R);
   using E = typename F::T;
@@ -249,11 +259,12 @@ template <class F> struct RDefault;
 // batch with plain twiddle loads (u32: R = 16 at 1024 threads/SM, C2 +5 %; the staged sub-problem
 // kernels measured 0.1-0.5 % faster with R = 8, profiles/r01h_sweep_u32_r16.txt)
 template <> struct RDefault<FieldU32> { static constexpr int RB = 8, RBF = 16, RC = 16; };
+template <> struct RDefault<FieldU32M> : RDefault<FieldU32> {};
 template <> struct RDefault<FieldGold> { static constexpr int RB = 8, RBF = 8, RC = 8; };
 template <> struct RDefault<FieldM31x2> { static constexpr int RB = 8, RBF = 8, RC = 8; };
 
 template <class F, int M>
-static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t st) {
+static int launch_block_r(const F& fld, const BlockKArgs<F>& args, cudaStream_t st) {
   // the application embeddings (fused path only) use one variant: the default R
   if (args.k == 0 && args.io.mode != EMB_PLAIN) return launch_block<F, M, RDefault<F>::RB, true>(fld, args, st);
   // latency-bound small fused batches (C1: one 1024-point product): 4 elements per thread, i.e.
@@ -285,7 +296,7 @@ static int launch_block_r(const F& fld, const BlockArgs<F>& args, cudaStream_t s
 //   inverse, 6 <= K < TMA_MIN_K -> k_cols_inv2 (two column groups per thread)   FCIRC_INV2=0 disables
 //   otherwise                   -> k_cols (R = 16, or the FCIRC_<field>_RC variant)
 template <class F, int K, bool INV>
-static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cudaStream_t st) {
+static int launch_cols_r(const F& fld, const ColKArgs<F>& args, int64_t inst, cudaStream_t st) {
   static const int use_tma = knob("TMA", 1);
   static const int use_fwd2 = knob("COLS2", 1);
   static const int r = knob(FTraits<F>::RC, RDefault<F>::RC);
@@ -335,7 +346,7 @@ static int launch_cols_r(const F& fld, const ColArgs<F>& args, int64_t inst, cud
 }
 
 template <class F, int... Ms>
-static int dispatch_block(int M, const F& fld, const BlockArgs<F>& args, cudaStream_t st,
+static int dispatch_block(int M, const F& fld, const BlockKArgs<F>& args, cudaStream_t st,
                           std::integer_sequence<int, Ms...>) {
   int rc = FCIRC_EINVAL;
   ((M == Ms ? (rc = launch_block_r<F, Ms>(fld, args, st), 0) : 0), ...);
@@ -343,7 +354,7 @@ static int dispatch_block(int M, const F& fld, const BlockArgs<F>& args, cudaStr
 }
 
 template <class F, bool INV, int... Ks>
-static int dispatch_cols(int K, const F& fld, const ColArgs<F>& args, int64_t inst, cudaStream_t st,
+static int dispatch_cols(int K, const F& fld, const ColKArgs<F>& args, int64_t inst, cudaStream_t st,
                          std::integer_sequence<int, Ks...>) {
   int rc = FCIRC_EINVAL;
   ((K == Ks + 1 ? (rc = launch_cols_r<F, Ks + 1, INV>(fld, args, inst, st), 0) : 0), ...);
@@ -361,9 +372,11 @@ static int msplit(int L) {
   return std::min(FTraits<F>::MMAX, std::max(pref, L - KMAX));
 }
 
+// mp (FieldU32M only): several primes in one launch per pass -- instance j of the
+// [batch][n] output belongs to prime j / mp->per and reads the operands of instance j % mp->per
 template <class F>
 static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
-                      int64_t batch, cudaStream_t st, int dev, const EmbedIO& io) {
+                      int64_t batch, cudaStream_t st, int dev, const EmbedIO& io, const MultiPrime* mp = nullptr) {
   using E = typename F::T;
   using Tw = typename F::Tw;
   const int MMAX = msplit<F>(L);
@@ -373,8 +386,11 @@ static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void
   if constexpr (sizeof(E) == 4) { lsi = dp.last_si32; lk = dp.last_k32; }
   else { lsi = dp.last_si64; lk = dp.last_k64; }
   const int64_t n = (int64_t)1 << L;
+  const MultiPrime mp1 = mp ? *mp : MultiPrime{};
   if (L <= MMAX) {
-    BlockArgs<F> ba{(const E*)a, (const E*)b, (E*)c, batch, 0, twf, twi, lsi, lk, io};
+    BlockKArgs<F> ba;
+    static_cast<BlockArgs<F>&>(ba) = BlockArgs<F>{(const E*)a, (const E*)b, (E*)c, batch, 0, twf, twi, lsi, lk, io};
+    if constexpr (kMulti<F>) ba.mp = mp1;
     return dispatch_block<F>(L, fld, ba, st, std::make_integer_sequence<int, FTraits<F>::MMAX + 1>{});
   }
   const int K = L - MMAX;
@@ -391,18 +407,28 @@ static int run_matvec(const F& fld, const DevPlan& dp, const void* a, const void
   const int64_t sa = plain ? n : io.na, sb = plain ? n : io.nb, sc = emb_truncates(io.mode) ? io.nc : n;
   for (int64_t i0 = 0; i0 < batch; i0 += C) {
     const int64_t cc = std::min<int64_t>(C, batch - i0);
-    const E* ai = (const E*)a + i0 * sa;
-    const E* bi = (const E*)b + i0 * sb;
+    // multi-prime launches index the caller's operands by the global instance (src_inst), so their
+    // source pointers are not advanced per chunk; the chunk's first global instance is mp.inst0
+    MultiPrime mpc = mp1;
+    mpc.inst0 = i0;
+    const E* ai = (const E*)a + (mp1.n > 1 ? 0 : i0 * sa);
+    const E* bi = (const E*)b + (mp1.n > 1 ? 0 : i0 * sb);
     E* ci = (E*)c + i0 * sc;
     E* ap = plain ? ci : (E*)ws;
     E* bw = plain ? (E*)ws : (E*)ws + C * n;
-    ColArgs<F> fa{ai, bi, ap, bw, n >> K, n, 0, 0, twf, twi, lsi, lk, io};
+    ColKArgs<F> fa;
+    static_cast<ColArgs<F>&>(fa) = ColArgs<F>{ai, bi, ap, bw, n >> K, n, 0, 0, twf, twi, lsi, lk, io};
+    if constexpr (kMulti<F>) fa.mp = mpc;
     rc = dispatch_cols<F, false>(K, fld, fa, cc, st, std::make_integer_sequence<int, KMAX>{});
     if (rc) return rc;
-    BlockArgs<F> ba{ap, bw, ap, cc << K, K, twf, twi, lsi, lk, EmbedIO{}};
+    BlockKArgs<F> ba;
+    static_cast<BlockArgs<F>&>(ba) = BlockArgs<F>{ap, bw, ap, cc << K, K, twf, twi, lsi, lk, EmbedIO{}};
+    if constexpr (kMulti<F>) ba.mp = mpc;
     rc = dispatch_block<F>(MMAX, fld, ba, st, std::make_integer_sequence<int, FTraits<F>::MMAX + 1>{});
     if (rc) return rc;
-    ColArgs<F> ia{ap, nullptr, ci, nullptr, n >> K, n, 0, 0, twf, twi, lsi, lk, io};
+    ColKArgs<F> ia;
+    static_cast<ColArgs<F>&>(ia) = ColArgs<F>{ap, nullptr, ci, nullptr, n >> K, n, 0, 0, twf, twi, lsi, lk, io};
+    if constexpr (kMulti<F>) ia.mp = mpc;
     rc = dispatch_cols<F, true>(K, fld, ia, cc, st, std::make_integer_sequence<int, KMAX>{});
     if (rc) return rc;
   }

@@ -66,8 +66,12 @@ size_t chunk_bytes();
 // a, b, c: device arrays laid out as io describes; c may not alias a or b.
 // io: EMB_PLAIN for fcirc_matvec; the applications pass their embedding (fcirc_kernels.cuh EmbedIO).
 struct EmbedIO;
+struct MultiPrime;
 int run_matvec_u32(const FieldU32& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
                    int64_t batch, cudaStream_t st, int dev, const EmbedIO& io);
+// several 32-bit primes in one launch per pass (fcirc_kernels.cuh MultiPrime): batch = mp.n * mp.per
+int run_matvec_u32m(const DevPlan& dp, const void* a, const void* b, void* c, int L, int64_t batch,
+                    cudaStream_t st, int dev, const EmbedIO& io, const MultiPrime& mp);
 int run_matvec_gold(const FieldGold& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,
                     int64_t batch, cudaStream_t st, int dev, const EmbedIO& io);
 int run_matvec_m31(const FieldM31x2& fld, const DevPlan& dp, const void* a, const void* b, void* c, int L,

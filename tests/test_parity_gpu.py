@@ -294,7 +294,11 @@ def _to_int(words):
 
 def test_bigint_small():
     rng = np.random.default_rng(88)
-    for nx, ny, batch in [(1, 1, 3), (1, 5, 2), (7, 3, 2), (64, 64, 2), (1000, 777, 2), (4096, 4096, 1)]:
+    # the three primes run as one launch per pass: odd batches and multi-pass sizes exercise the
+    # per-CTA prime selection (staged sub-problems) and the per-thread one (fused, several instances
+    # per CTA straddling primes)
+    for nx, ny, batch in [(1, 1, 3), (1, 5, 2), (7, 3, 2), (9, 9, 7), (64, 64, 2), (200, 100, 5), (1000, 777, 2),
+                          (4096, 4096, 1), (5000, 5000, 5), (20000, 3000, 3)]:
         inp = synth.bigint_inputs(max(nx, ny), batch, seed=int(rng.integers(1 << 30)))
         x = np.ascontiguousarray(inp["x"][:, :nx])
         y = np.ascontiguousarray(inp["y"][:, :ny])
