@@ -208,19 +208,32 @@ __device__ __forceinline__ int64_t src_inst(const A& args, int64_t inst) {
 // holds in phase ph_to and the next exchange (from ph_to) writes exactly those addresses, so it
 // only overwrites values it has already read itself.  Callers that reuse the buffer with another
 // layout (k_cols_tma between tiles) synchronise themselves.
-template <class PH, int R, class T, class Idx>
-__device__ __forceinline__ void exchange(T (&x)[R], T* buf, int ph_from, int ph_to, int t, Idx idx) {
+// barrier of an exchange: the whole CTA, or (k_block_pipe) one named barrier per independent
+// thread group of a CTA
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct NamedSync {
+  int id, nthreads;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  }
+};
+
+template <class PH, int R, class T, class Idx, class Sync = CtaSync>
+__device__ __forceinline__ void exchange(T (&x)[R], T* buf, int ph_from, int ph_to, int t, Idx idx, Sync sync = Sync{}) {
   const int wb = PH::ins_t(ph_from, t);
 #pragma unroll
   for (int s = 0; s < R; ++s) buf[idx(wb, PH::cslot(ph_from, s))] = x[s];
-  __syncthreads();
+  sync();
   const int rb = PH::ins_t(ph_to, t);
 #pragma unroll
   for (int s = 0; s < R; ++s) x[s] = buf[idx(rb, PH::cslot(ph_to, s))];
 }
 
-template <class PH, int R, class T, class Idx>
-__device__ __forceinline__ void exchange2(T (&x)[R], T (&y)[R], T* bx, T* by, int ph_from, int ph_to, int t, Idx idx) {
+template <class PH, int R, class T, class Idx, class Sync = CtaSync>
+__device__ __forceinline__ void exchange2(T (&x)[R], T (&y)[R], T* bx, T* by, int ph_from, int ph_to, int t, Idx idx,
+                                          Sync sync = Sync{}) {
   const int wb = PH::ins_t(ph_from, t);
 #pragma unroll
   for (int s = 0; s < R; ++s) {
@@ -228,13 +241,36 @@ __device__ __forceinline__ void exchange2(T (&x)[R], T (&y)[R], T* bx, T* by, in
     bx[ad] = x[s];
     by[ad] = y[s];
   }
-  __syncthreads();
+  sync();
   const int rb = PH::ins_t(ph_to, t);
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     const int ad = idx(rb, PH::cslot(ph_to, s));
     x[s] = bx[ad];
     y[s] = by[ad];
+  }
+}
+
+// In-warp alternative to the LAST exchange (phases NPH-2 <-> NPH-1 of a 2^M-point transform with
+// R = 2^r points per thread): there the exchanged address bits are the low r thread bits, i.e. lanes
+// of one group of R consecutive lanes, and the exchange is an R x R transpose within each group:
+// r butterfly stages of __shfl_xor_sync (stage k swaps the slots whose bit k differs from the lane's
+// bit k with lane ^ 2^k), no shared memory and no barrier.  (North-star mechanism "warp-shuffle
+// exchanges for the innermost levels"; measured against the shared-memory exchange.)
+template <int R, class T>
+__device__ __forceinline__ void lane_transpose(T (&x)[R], int lane) {
+#pragma unroll
+  for (int k = 0; (1 << k) < R; ++k) {
+    const int b = 1 << k;
+    const bool upper = (lane >> k) & 1;
+#pragma unroll
+    for (int s0 = 0; s0 < R; ++s0) {
+      if (s0 & b) continue;
+      const T send = upper ? x[s0] : x[s0 | b];
+      const T recv = __shfl_xor_sync(0xffffffffu, send, b);
+      if (upper) x[s0] = recv;
+      else x[s0 | b] = recv;
+    }
   }
 }
 
@@ -314,7 +350,7 @@ template <class F, int M> struct TwStage { static constexpr bool value = false; 
 template <int M> struct TwStage<FieldU32, M> { static constexpr bool value = M >= 6; };
 template <int M> struct TwStage<FieldU32M, M> { static constexpr bool value = M >= 6; };
 
-template <class F, int M, int R, int IPC, int MINB = 1, bool EMB = false, bool TWS = false>
+template <class F, int M, int R, int IPC, int MINB = 1, bool EMB = false, bool TWS = false, bool SHF = false>
 __global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
 k_block(F fld0, BlockKArgs<F> args) {
   using T = typename F::T;
@@ -404,9 +440,20 @@ k_block(F fld0, BlockKArgs<F> args) {
   }
 
   // ---- forward levels (Algorithm 1 split of a and b, sharing each twiddle), phase by phase
+  static_assert(!SHF || (NPH >= 2 && PH::rp(NPH - 2) == PH::r && PH::lo(NPH - 2) == PH::r),
+                "lane_transpose needs full-width last two phases");
 #pragma unroll
   for (int ph = 0; ph < NPH; ++ph) {
-    if (ph > 0) exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx);
+    if constexpr (SHF && NPH >= 2) {
+      if (ph == NPH - 1) {
+        lane_transpose<R>(xa, t & (R - 1));
+        lane_transpose<R>(xb, t & (R - 1));
+      } else if (ph > 0) {
+        exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx);
+      }
+    } else {
+      if (ph > 0) exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx);
+    }
     forward_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
       const Tw tw = tw_at(view_twf<F>(fv, args), twsf, bit, tb, cs);
       fld.fwd_a(xa[s0], xa[s1], tw);
@@ -430,7 +477,12 @@ k_block(F fld0, BlockKArgs<F> args) {
     const bool top = (k == 0);
 #pragma unroll
     for (int ph = NPH - 1; ph >= 0; --ph) {
-      if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx);
+      if constexpr (SHF && NPH >= 2) {
+        if (ph == NPH - 2) lane_transpose<R>(xm, t & (R - 1));
+        else if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx);
+      } else {
+        if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx);
+      }
       inverse_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
         if (bit == M - 1 && top) fld.inv_last(xm[s0], xm[s1], view_lsi<F>(fv, args), view_lk<F>(fv, args));
         else fld.inv(xm[s0], xm[s1], tw_at(view_twi<F>(fv, args), twsi, bit, tb, cs));
@@ -639,7 +691,12 @@ k_cols_fwd2(F fld0, ColKArgs<F> args) {
 // k_cols_inv2: the inverse column pass with two column groups (c and c + W) per thread, sharing
 // every twiddle load and doubling the independent butterflies per level (plain operands).
 // ------------------------------------------------------------------------------------------
-template <class F, int K, int R, int W, int MINB = 1, bool EMB = false>
+// VEC: the two column groups of a thread are ADJACENT columns (2c, 2c+1), read and written as one
+// 2-element vector access (16 bytes for Goldilocks) instead of two scalar accesses at c and c + W.
+template <class T> struct Vec2;
+template <> struct Vec2<uint32_t> { using type = uint2; };
+template <> struct Vec2<uint64_t> { using type = ulonglong2; };
+template <class F, int K, int R, int W, int MINB = 1, bool EMB = false, bool VEC = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols_inv2(F fld0, ColKArgs<F> args) {
   using T = typename F::T;
@@ -653,18 +710,25 @@ k_cols_inv2(F fld0, ColKArgs<F> args) {
   const int c = threadIdx.x % W;
   const int t = threadIdx.x / W;
   const int64_t inst = blockIdx.x / args.colblocks;     // colblocks = m / (2 W)
-  const int64_t base = inst * args.n + (blockIdx.x - inst * args.colblocks) * 2 * W + c;
+  const int64_t base = inst * args.n + (blockIdx.x - inst * args.colblocks) * 2 * W + (VEC ? 2 * c : c);
   const int64_t m = args.m;
   const ColIdx<PH, W> idx{c};
   const auto fv = field_view(fld0, args, inst);
   const F& fld = select_field(fv, fld0);
+  using V2 = typename Vec2<T>::type;
 
   T xa[R], xb[R];
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     const int64_t ad = base + (int64_t)(PH::ins_t(NPH - 1, t) + PH::cslot(NPH - 1, s)) * m;
-    xa[s] = args.src0[ad];
-    xb[s] = args.src0[ad + W];
+    if constexpr (VEC) {
+      const V2 v = *reinterpret_cast<const V2*>(args.src0 + ad);
+      xa[s] = v.x;
+      xb[s] = v.y;
+    } else {
+      xa[s] = args.src0[ad];
+      xb[s] = args.src0[ad + W];
+    }
   }
   col_inverse<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
     if (bit == K - 1) {
@@ -688,8 +752,12 @@ k_cols_inv2(F fld0, ColKArgs<F> args) {
 #pragma unroll
     for (int s = 0; s < R; ++s) {
       const int64_t ad = base + (int64_t)(PH::ins_t(0, t) + PH::cslot(0, s)) * m;
-      args.dst0[ad] = xa[s];
-      args.dst0[ad + W] = xb[s];
+      if constexpr (VEC) {
+        *reinterpret_cast<V2*>(args.dst0 + ad) = V2{xa[s], xb[s]};
+      } else {
+        args.dst0[ad] = xa[s];
+        args.dst0[ad + W] = xb[s];
+      }
     }
   }
 }
@@ -817,6 +885,125 @@ k_cols_tma(F fld0, ColKArgs<F> args, const __grid_constant__ CUtensorMap map0, c
 #pragma unroll
     for (int s = 0; s < R; ++s) dst[base + (int64_t)(PH::ins_t(ph_out, t) + PH::cslot(ph_out, s)) * m] = x[s];
     __syncthreads();   // stage st and the exchange buffer are free for the next issue / tile
+  }
+}
+
+
+// ------------------------------------------------------------------------------------------
+// k_block_pipe: the 32-bit sub-problem kernel with its operand loads taken off the critical path.
+//
+// One CTA per SM of 2 x (2^M / R) threads: two independent halves share the staged twiddle slice
+// of sub-block E and each walks its own sequence of instances of E.  A half's
+// a' and b' slices (2^M contiguous elements each) are brought into a shared-memory stage by the
+// Tensor Memory Accelerator's bulk copy (cp.async.bulk, mbarrier with the byte count) one
+// instance AHEAD: while the half transforms instance j from registers, the copy of instance j + 1
+// is in flight, so the global-load latency that stalled k_block at every instance start
+// (long_scoreboard, profiles/r01n_ncu_full_S1.txt) overlaps the arithmetic.  The halves synchronise
+// their exchanges with their own named barriers (bar.sync 1 / 2), so one never waits for the other.
+// Shared memory: twiddles 2 x 2^M Tw + per half (stage 2 x 2^M T, exchange 2 x 2^M T) + mbarriers.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <class F, int M, int R>
+__global__ void __launch_bounds__(2 * (1 << M) / R, 1)
+k_block_pipe(F fld0, BlockKArgs<F> args) {
+  using T = typename F::T;
+  using Tw = typename F::Tw;
+  using PH = Phases<M, R>;
+  constexpr int m = 1 << M;
+  constexpr int TT = PH::T;
+  constexpr int NPH = PH::NPH;
+  constexpr uint32_t SLICE = (uint32_t)(m * sizeof(T));
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Tw* twsf = reinterpret_cast<Tw*>(smem_raw);
+  Tw* twsi = twsf + m;
+  const int half = threadIdx.x / TT;
+  const int t = threadIdx.x % TT;
+  T* stage_a = reinterpret_cast<T*>(twsi + m) + (size_t)half * 4 * m;   // [stage a | stage b | xa | xb]
+  T* stage_b = stage_a + m;
+  T* sa = stage_a + 2 * m;
+  T* sb = stage_a + 3 * m;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<T*>(twsi + m) + (size_t)8 * m);
+  const NamedSync hsync{1 + half, TT};
+  auto idx = [](int base_part, int slot_part) { return swz<R, T>(base_part) ^ swz<R, T>(slot_part); };
+
+  const int k = args.k;
+  const int64_t batch = args.units >> k;
+  const int nseq = args.seq;                         // instances per half
+  const int E = (int)(blockIdx.x & ((1u << k) - 1));
+  const int64_t first = (int64_t)(blockIdx.x >> k) * 2 * nseq;   // the CTA's first instance
+  const auto fv = field_view(fld0, args, first);     // one prime per CTA (launcher)
+  const F& fld = select_field(fv, fld0);
+  auto inst_of = [&](int j) { return first + 2 * (int64_t)j + half; };
+  auto src_a = [&](int64_t inst) { return args.a + ((inst << k) + E) * (int64_t)m; };
+  auto src_b = [&](int64_t inst) { return args.b + ((inst << k) + E) * (int64_t)m; };
+  auto issue = [&](int64_t inst) {
+    mbar_expect_tx(&bars[half], 2 * SLICE);
+    bulk_load(stage_a, src_a(inst), SLICE, &bars[half]);
+    bulk_load(stage_b, src_b(inst), SLICE, &bars[half]);
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // twiddle slice of sub-block E (all threads), as k_block's staging
+  for (int h = threadIdx.x + 1; h < m; h += blockDim.x) {
+    const int j = 31 - __clz(h);
+    const int g = (1 << (k + j)) + (E << j) + (h - (1 << j));
+    twsf[tw_swz(h)] = view_twf<F>(fv, args)[g];
+    twsi[tw_swz(h)] = view_twi<F>(fv, args)[g];
+  }
+  __syncthreads();
+  if (t == 0 && inst_of(0) < batch) issue(inst_of(0));
+
+  auto tw_st = [&](const Tw* staged, int bit, int tb, int cs) -> Tw {
+    return staged[tw_swz(1 << (M - 1 - bit)) ^ tw_swz(tb >> (bit + 1)) ^ tw_swz(cs >> (bit + 1))];
+  };
+  for (int j = 0; j < nseq; ++j) {
+    const int64_t inst = inst_of(j);
+    if (inst >= batch) break;                         // uniform per half
+    mbar_wait(&bars[half], (uint32_t)(j & 1));
+    T xa[R], xb[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
+      xa[s] = stage_a[ad];
+      xb[s] = stage_b[ad];
+    }
+    hsync();                                          // the half has read the stage: refill it
+    if (t == 0 && inst_of(j + 1) < batch && j + 1 < nseq) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(inst_of(j + 1));
+    }
+#pragma unroll
+    for (int ph = 0; ph < NPH; ++ph) {
+      if (ph > 0) exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx, hsync);
+      forward_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
+        const Tw tw = tw_st(twsf, bit, tb, cs);
+        fld.fwd_a(xa[s0], xa[s1], tw);
+        fld.fwd_b(xb[s0], xb[s1], tw);
+      });
+    }
+    T xm[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) xm[s] = fld.leaf(xa[s], xb[s]);
+#pragma unroll
+    for (int ph = NPH - 1; ph >= 0; --ph) {
+      if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx, hsync);
+      inverse_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
+        fld.inv(xm[s0], xm[s1], tw_st(twsi, bit, tb, cs));
+      });
+    }
+    T* out = args.out + ((inst << k) + E) * (int64_t)m;
+#pragma unroll
+    for (int s = 0; s < R; ++s) out[PH::ins_t(0, t) + PH::cslot(0, s)] = xm[s];
   }
 }
 

@@ -64,12 +64,49 @@ template <int RR> constexpr int wsel(int K) {
   return (256 * rsel<RR>(K)) >> K < 8 ? 8 : ((256 * rsel<RR>(K)) >> K);
 }
 
+// k_block_pipe (32-bit fields, staged sub-problem launches of 2^12 points at R = 8): two instance
+// streams per CTA with bulk-copy prefetch of the next instance's operands (fcirc_kernels.cuh).
+// FCIRC_U32_PIPE=0 disables it; FCIRC_U32_PSEQ = instances per half (default 8).
+template <class F, int M, int R>
+static int launch_block_pipe(const F& fld, const BlockKArgs<F>& args, cudaStream_t st) {
+  using E = typename F::T;
+  using Tw = typename F::Tw;
+  constexpr int T = (1 << M) / R;
+  const size_t smem = (size_t)2 * (1 << M) * sizeof(Tw) + (size_t)8 * (1 << M) * sizeof(E) + 16;
+  auto kern = k_block_pipe<F, M, R>;
+  static std::atomic<uint32_t> attr_mask{0};
+  if (!smem_optin((const void*)kern, smem, attr_mask)) return FCIRC_ECUDA;
+  const int64_t batch = args.units >> args.k;
+  static const int knob_seq = std::max(1, knob("U32_PSEQ", 8));
+  int seq = 1;
+  while (seq * 2 <= knob_seq && 2 * seq * 2 <= batch) seq *= 2;
+  if constexpr (kMulti<F>)   // the CTA's 2 seq instances inside one prime
+    while (seq > 1 && (args.mp.per % (2 * seq) != 0 || args.mp.inst0 % (2 * seq) != 0)) seq >>= 1;
+  BlockKArgs<F> a2 = args;
+  a2.seq = seq;
+  const int64_t grid = ((batch + 2 * seq - 1) / (2 * seq)) << args.k;
+  prof_begin(1, st);
+  kern<<<(unsigned)grid, 2 * T, smem, st>>>(fld, a2);
+  prof_end(st);
+  count_launch();
+  return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
+}
+
 template <class F, int M, int RR, bool EMB, bool TWS>
 static int launch_block_t(const F& fld, const BlockKArgs<F>& args, cudaStream_t st) {
   constexpr int R = rsel<RR>(M), IPC = ipcsel<RR>(M);
   constexpr int T = (1 << M) / R;
   using E = typename F::T;
   constexpr int PM = 1 << M;  // swizzled, unpadded (fcirc_kernels.cuh swz)
+  if constexpr (TWS && !EMB && sizeof(E) == 4 && M == 12 && R == 8) {
+    // measured against this kernel: S1 +1.3 %, C3 -4..8 %, C5 +-0 (profiles/r02d_ab_pipe.txt): off
+    // by default
+    static const int use_pipe = knob("U32_PIPE", 0);
+    const bool aligned = ((uintptr_t)args.a & 15) == 0 && ((uintptr_t)args.b & 15) == 0;
+    bool pairs_in_one_prime = true;   // a CTA's two halves start in one prime
+    if constexpr (kMulti<F>) pairs_in_one_prime = args.mp.per % 2 == 0 && args.mp.inst0 % 2 == 0;
+    if (use_pipe && args.k > 0 && aligned && pairs_in_one_prime) return launch_block_pipe<F, M, R>(fld, args, st);
+  }
   const size_t smem = (size_t)IPC * 2 * PM * sizeof(E) + (TWS ? (size_t)2 * (1 << M) * sizeof(typename F::Tw) : 0);
   // occupancy target: 1024 resident threads per SM (register cap 64) for R <= 8, and for R = 16
   // with 32-bit elements when the twiddles are not staged (plain loads, M = 12: fits 64 registers
@@ -79,8 +116,15 @@ static int launch_block_t(const F& fld, const BlockKArgs<F>& args, cudaStream_t 
   constexpr int TGT = (RR <= 8 || (sizeof(E) == 4 && !TWS && !EMB && M == 12)) ? 1024 : 512;
   constexpr int MINB = (T * IPC < TGT) ? TGT / (T * IPC) : 1;
   auto kern = k_block<F, M, R, IPC, MINB, EMB, TWS>;
-  static std::atomic<uint32_t> attr_mask{0};   // opt-in shared memory once per (kernel, device)
-  if (!smem_optin((const void*)kern, smem, attr_mask)) return FCIRC_ECUDA;
+  if constexpr (M == 12 && R == 8 && !EMB) {
+    // FCIRC_SHFL=1: the last exchange of sub-problem launches as an in-warp lane transpose (A/B only;
+    // measured slower)
+    static const int shf = knob("SHFL", 0);
+    if (shf && args.k > 0) kern = k_block<F, M, R, IPC, MINB, EMB, TWS, true>;
+  }
+  static std::atomic<uint32_t> attr_mask[2];   // opt-in shared memory once per (kernel, device)
+  if (!smem_optin((const void*)kern, smem, attr_mask[kern == k_block<F, M, R, IPC, MINB, EMB, TWS> ? 0 : 1]))
+    return FCIRC_ECUDA;
   const int64_t batch = args.units >> args.k;
   BlockKArgs<F> a2 = args;
   // staged sub-problem launches: each CTA walks seq instance groups of one sub-block, staging its
@@ -178,8 +222,17 @@ static int launch_cols_inv2(const F& fld, ColKArgs<F> args, int64_t instances, c
   const size_t smem = (size_t)2 * (1 << K) * W * sizeof(E);
   constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
   auto kern = k_cols_inv2<F, K, R, W, MINB, EMB>;
-  static std::atomic<uint32_t> attr_mask{0};   // opt-in shared memory once per (kernel, device)
-  if (!smem_optin((const void*)kern, smem, attr_mask)) return FCIRC_ECUDA;
+  if constexpr (!EMB) {
+    // adjacent column pairs as one 2-element vector access (16 bytes for the 8-byte fields; the
+    // north-star's 128-bit accesses): measured equal to the scalar pair at C4 n = 2^20
+    // (profiles/r02e_gold_ab_shfl_vec.txt), default on when the base is 16-byte aligned
+    static const int vec = knob("VEC", 1);
+    if (vec && ((uintptr_t)args.src0 & 15) == 0 && ((uintptr_t)args.dst0 & 15) == 0)
+      kern = k_cols_inv2<F, K, R, W, MINB, EMB, true>;
+  }
+  static std::atomic<uint32_t> attr_mask[2];   // opt-in shared memory once per (kernel, device)
+  if (!smem_optin((const void*)kern, smem, attr_mask[kern == k_cols_inv2<F, K, R, W, MINB, EMB> ? 0 : 1]))
+    return FCIRC_ECUDA;
   args.colblocks = args.m / (2 * W);
   args.units = instances * args.colblocks;
   prof_begin(3, st);

@@ -163,6 +163,16 @@ void run_block(const Bufs& B, cudaStream_t st) {
   kern<<<(unsigned)(INST << K), (1 << M) / R, smem, st>>>(F{}, ba);
 }
 template <int V>
+void run_block_shf(const Bufs& B, cudaStream_t st) {
+  using F = GV<V>;
+  BlockArgs<F> ba{B.a, B.b, B.out, (int64_t)INST << K, K, B.twf, B.twi, 0, 0, EmbedIO{}};
+  auto kern = k_block<F, M, R, 1, 2, false, false, true>;
+  const size_t smem = 2 * (1 << M) * 8;
+  static bool once = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
+  (void)once;
+  kern<<<(unsigned)(INST << K), (1 << M) / R, smem, st>>>(F{}, ba);
+}
+template <int V>
 void run_fwd(const Bufs& B, cudaStream_t st) {
   using F = GV<V>;
   ColArgs<F> ca{B.a, B.b, B.out, B.ob, N >> K, N, 0, 0, B.twf, B.twi, 0, 0, EmbedIO{}};
@@ -182,6 +192,15 @@ void run_inv(const Bufs& B, cudaStream_t st) {
 }
 
 template <int V>
+void run_inv_vec(const Bufs& B, cudaStream_t st) {
+  using F = GV<V>;
+  ColArgs<F> ca{B.a, nullptr, B.out, nullptr, N >> K, N, 0, 0, B.twf, B.twi, 12345, 678, EmbedIO{}};
+  ca.colblocks = ca.m / (2 * W);
+  ca.units = INST * ca.colblocks;
+  k_cols_inv2<F, K, R, W, 4, false, true><<<(unsigned)ca.units, W * ((1 << K) / R), 2 * (1 << K) * W * 8, st>>>(F{}, ca);
+}
+
+template <int V>
 void bench(const char* name, int reps, const Bufs& B, std::vector<uint64_t>* ref_blk, std::vector<uint64_t>* ref_fwd,
            std::vector<uint64_t>* ref_inv) {
   const size_t ne = (size_t)INST * N;
@@ -189,6 +208,10 @@ void bench(const char* name, int reps, const Bufs& B, std::vector<uint64_t>* ref
   float tb = time_launches<GV<V>>(reps, run_block<V>, B);
   CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
   bool okb = ref_blk->empty() ? (*ref_blk = h, true) : (*ref_blk == h);
+  float ts = time_launches<GV<V>>(reps, run_block_shf<V>, B);
+  CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
+  printf("{\"variant\": %d, \"k_block_lane_transpose_ms\": %.4f, \"k_block_smem_exchange_ms\": %.4f, \"match\": %d}\n",
+         V, ts, tb, (int)(*ref_blk == h));
   float tf = time_launches<GV<V>>(reps, run_fwd<V>, B);
   CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(h2.data(), B.ob, ne * 8, cudaMemcpyDeviceToHost));
@@ -198,6 +221,10 @@ void bench(const char* name, int reps, const Bufs& B, std::vector<uint64_t>* ref
   h.resize(ne);
   CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
   bool oki = ref_inv->empty() ? (*ref_inv = h, true) : (*ref_inv == h);
+  float tv = time_launches<GV<V>>(reps, run_inv_vec<V>, B);
+  CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
+  const bool okv = *ref_inv == h;
+  printf("{\"variant\": %d, \"k_cols_inv2_vec16_ms\": %.4f, \"k_cols_inv2_scalar_ms\": %.4f, \"match\": %d}\n", V, tv, ti, okv);
   printf("{\"variant\": %d, \"name\": \"%s\", \"k_block_ms\": %.4f, \"k_cols_fwd2_ms\": %.4f, \"k_cols_inv2_ms\": %.4f, "
          "\"sum_ms\": %.4f, \"match\": [%d, %d, %d]}\n", V, name, tb, tf, ti, tb + tf + ti, okb, okf, oki);
   fflush(stdout);
@@ -226,8 +253,7 @@ int main(int argc, char** argv) {
   for (int round = 0; round < 2; ++round) {   // two rounds: A B A B
     bench<0>("round-1 reduce", reps, B, &rb, &rf, &ri);
     bench<1>("wide-eps reduce", reps, B, &rb, &rf, &ri);
-    bench<3>("explicit mul.wide product + wide-eps reduce", reps, B, &rb, &rf, &ri);
-    bench<4>("explicit mul.wide product + round-1 reduce", reps, B, &rb, &rf, &ri);
+
   }
   return 0;
 }
