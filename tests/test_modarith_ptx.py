@@ -4,7 +4,7 @@ The chains are executed by tools/ptx_carry_sim.py under the hardware carry model
 its docstring) on edge and random operands and compared with Python integers.  This pins the
 contracts the kernels rely on: add_c(weak, canonical) and sub_c(weak, canonical)
 need one correction, sub_w(weak, weak) two, and the 128 -> 64 reduction returns the canonical
-residue.  A GPU re-check of the same helpers runs in tools/gold_bench.cu.
+residue.  The GPU side: every kernel variant's output is compared bit for bit in tools/gold_ab.cu.
 """
 import os
 import random
