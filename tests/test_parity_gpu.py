@@ -569,3 +569,52 @@ def test_host_pipeline_concurrent_threads():
     assert not errors, errors
     for (tid, j), (inp, c) in res.items():
         check_sampled(inp, c, range(inp["batch"]), name=f"host pipeline thread {tid} call {j}")
+
+
+def test_outputs_stay_inside_their_buffers():
+    """Own bounds check (compute-sanitizer is closed on this pool): every output is written into the
+    middle of a larger buffer whose guard bands hold a sentinel; after the call the guards must be
+    untouched and the product exact -- fused, multi-pass (incl. the TMA and vector column paths),
+    truncating polymul stores, any-n circulants and bigint."""
+    G = 4096   # guard elements on each side
+
+    def guarded(shape, dtype):
+        n = int(np.prod(shape))
+        store = torch.full((n + 2 * G,), 0x5A5A5A5A, dtype=dtype, device="cuda")
+        return store, store[G:G + n].view(*shape)
+
+    def guards_intact(store):
+        g = store.cpu().numpy()
+        return bool((g[:G] == 0x5A5A5A5A).all() and (g[-G:] == 0x5A5A5A5A).all())
+
+    for p, L, batch in [(GOLDILOCKS, 10, 3), (GOLDILOCKS, 16, 2), (GOLDILOCKS, 21, 1), (P998, 12, 5), (P998, 17, 3)]:
+        inp = synth.matvec_inputs(p, 1 << L, batch, seed=8000 + L)
+        dt = torch.int64 if p == GOLDILOCKS else torch.int32
+        store, out = guarded((batch, 1 << L), dt)
+        fc.matvec(_dev(inp["a"]), _dev(inp["b"]), inp["f"], p, out=out)
+        torch.cuda.synchronize()
+        assert guards_intact(store), (p, L)
+        check_sampled(inp, _host(out), range(batch), name=f"guarded p={p} n=2^{L}")
+    for na, nb in [(700, 300), (9000, 7000)]:
+        pin = synth.polymul_inputs(P998, na, nb, 2, seed=na)
+        store, out = guarded((2, na + nb - 1), torch.int32)
+        fc.polymul(_dev(pin["a"]), _dev(pin["b"]), P998, out=out)
+        torch.cuda.synchronize()
+        assert guards_intact(store), (na, nb)
+        for k in range(2):
+            assert np.array_equal(_host(out)[k].astype(np.uint32).astype(np.uint64),
+                                  oracle.polymul_coeffs(P998, pin["a"][k], pin["b"][k]))
+    for n in [1000, 5000]:
+        inp = synth.matvec_inputs(P998, n, 2, seed=n, f_mode="one")
+        store, out = guarded((2, n), torch.int32)
+        fc.circulant_matvec(_dev(inp["a"]), _dev(inp["b"]), P998, out=out)
+        torch.cuda.synchronize()
+        assert guards_intact(store), n
+    bi = synth.bigint_inputs(3000, 3, seed=4)
+    store, out = guarded((3, 6000), torch.int32)
+    fc.bigint_mul(_dev(bi["x"]), _dev(bi["y"]), out=out)
+    torch.cuda.synchronize()
+    assert guards_intact(store)
+    z = _host(out).astype(np.uint32)
+    for k in range(3):
+        assert _to_int(z[k]) == _to_int(bi["x"][k]) * _to_int(bi["y"][k])
