@@ -311,7 +311,7 @@ template <class F> struct RDefault;
 // RB: sub-problem launches (and the staged-twiddle small fused ones); RBF: fused launches of a large
 // batch with plain twiddle loads (u32: R = 16 at 1024 threads/SM, C2 +5 %; the staged sub-problem
 // kernels measured 0.1-0.5 % faster with R = 8, profiles/r01h_sweep_u32_r16.txt)
-template <> struct RDefault<FieldU32> { static constexpr int RB = 8, RBF = 16, RC = 16; };
+template <> struct RDefault<FieldU32> { static constexpr int RB = 16, RBF = 16, RC = 16; };   // RB 16: r02i re-sweep
 template <> struct RDefault<FieldU32M> : RDefault<FieldU32> {};
 template <> struct RDefault<FieldGold> { static constexpr int RB = 8, RBF = 8, RC = 8; };
 template <> struct RDefault<FieldM31x2> { static constexpr int RB = 8, RBF = 8, RC = 8; };

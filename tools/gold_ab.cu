@@ -106,14 +106,32 @@ struct GV : FieldGold {
     const uint64_t lo = a * b, hi = __umul64hi(a, b);
     return red(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
   }
+  // V == 5: a + b mod p with the carry correction +c*EPS as ONE IMAD.WIDE.U32 (c * 0xffffffff + s),
+  // moving it from the ALU pipe (ISETP + two predicated adds) to the FMA pipe
+  __device__ __forceinline__ static uint64_t addc_v(uint64_t a, uint64_t b) {
+    if constexpr (V == 5) {
+      uint64_t r;
+      asm("{\n\t.reg .u32 s0, s1, c;\n\t.reg .u64 S, E;\n\t"
+          "add.cc.u32  s0, %1, %3;\n\t"
+          "addc.cc.u32 s1, %2, %4;\n\t"
+          "addc.u32    c, 0, 0;\n\t"
+          "mov.b64     S, {s0, s1};\n\t"
+          "mul.wide.u32 E, c, 0xffffffff;\n\t"
+          "add.u64     %0, S, E;\n\t}"
+          : "=l"(r) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+      return r;
+    } else {
+      return add_c(a, b);
+    }
+  }
   __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
-    const uint64_t t = mul(y, s); const uint64_t X = x; x = add_c(X, t); y = sub_c(X, t);
+    const uint64_t t = mul(y, s); const uint64_t X = x; x = addc_v(X, t); y = sub_c(X, t);
   }
   __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
-    const uint64_t t = mul(x, s); const uint64_t Y = y; x = add_c(Y, t); y = sub_w(t, Y);
+    const uint64_t t = mul(x, s); const uint64_t Y = y; x = addc_v(Y, t); y = sub_w(t, Y);
   }
   __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
-    const uint64_t s = add_c(u, v); const uint64_t d = sub_c(u, v); u = mul(s, si); v = d;
+    const uint64_t s = addc_v(u, v); const uint64_t d = sub_c(u, v); u = mul(s, si); v = d;
   }
   __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
     const uint64_t s = add_c(u, v); const uint64_t d = sub_c(u, v); u = mul(s, si_k); v = mul(d, k);
@@ -253,6 +271,7 @@ int main(int argc, char** argv) {
   for (int round = 0; round < 2; ++round) {   // two rounds: A B A B
     bench<0>("round-1 reduce", reps, B, &rb, &rf, &ri);
     bench<1>("wide-eps reduce", reps, B, &rb, &rf, &ri);
+    bench<5>("wide-eps reduce + add_c correction as IMAD.WIDE", reps, B, &rb, &rf, &ri);
 
   }
   return 0;
