@@ -220,7 +220,10 @@ static int launch_cols_inv2(const F& fld, ColKArgs<F> args, int64_t instances, c
   constexpr int threads = W * ((1 << K) / R);
   using E = typename F::T;
   const size_t smem = (size_t)2 * (1 << K) * W * sizeof(E);
-  constexpr int MINB = (threads < (RR <= 8 ? 1024 : 512)) ? (RR <= 8 ? 1024 : 512) / threads : 1;
+  // 32-bit R = 16: 768 resident threads (<= 85 registers) instead of 512 (96 registers, 23 % of the
+  // warp slots active, latency-bound: profiles/r02f_ncu_full_S1.txt)
+  constexpr int TGT = RR <= 8 ? 1024 : (sizeof(E) == 4 ? 768 : 512);
+  constexpr int MINB = (threads < TGT) ? TGT / threads : 1;
   auto kern = k_cols_inv2<F, K, R, W, MINB, EMB>;
   if constexpr (!EMB) {
     // adjacent column pairs as one 2-element vector access (16 bytes for the 8-byte fields; the
