@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -209,6 +210,31 @@ void run_inv(const Bufs& B, cudaStream_t st) {
   k_cols_inv2<F, K, R, W, 4, false><<<(unsigned)ca.units, W * ((1 << K) / R), 2 * (1 << K) * W * 8, st>>>(F{}, ca);
 }
 
+template <int V, int WW>
+void run_fwd_w(const Bufs& B, cudaStream_t st) {
+  using F = GV<V>;
+  ColArgs<F> ca{B.a, B.b, B.out, B.ob, N >> K, N, 0, 0, B.twf, B.twi, 0, 0, EmbedIO{}};
+  ca.colblocks = ca.m / WW;
+  ca.units = INST * ca.colblocks;
+  auto kern = k_cols_fwd2<F, K, R, WW, (1024 / (WW * ((1 << K) / R))) < 1 ? 1 : 1024 / (WW * ((1 << K) / R)), false>;
+  const size_t smem = 2 * (1 << K) * WW * 8;
+  static bool once = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
+  (void)once;
+  kern<<<(unsigned)ca.units, WW * ((1 << K) / R), smem, st>>>(F{}, ca);
+}
+template <int V, int WW>
+void run_inv_w(const Bufs& B, cudaStream_t st) {
+  using F = GV<V>;
+  ColArgs<F> ca{B.a, nullptr, B.out, nullptr, N >> K, N, 0, 0, B.twf, B.twi, 12345, 678, EmbedIO{}};
+  ca.colblocks = ca.m / (2 * WW);
+  ca.units = INST * ca.colblocks;
+  auto kern = k_cols_inv2<F, K, R, WW, (1024 / (WW * ((1 << K) / R))) < 1 ? 1 : 1024 / (WW * ((1 << K) / R)), false, true>;
+  const size_t smem = 2 * (1 << K) * WW * 8;
+  static bool once = (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), true);
+  (void)once;
+  kern<<<(unsigned)ca.units, WW * ((1 << K) / R), smem, st>>>(F{}, ca);
+}
+
 template <int V>
 void run_inv_vec(const Bufs& B, cudaStream_t st) {
   using F = GV<V>;
@@ -239,6 +265,16 @@ void bench(const char* name, int reps, const Bufs& B, std::vector<uint64_t>* ref
   h.resize(ne);
   CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
   bool oki = ref_inv->empty() ? (*ref_inv = h, true) : (*ref_inv == h);
+  {
+    float tf16 = time_launches<GV<V>>(reps, run_fwd_w<V, 16>, B);
+    CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
+    const bool okf16 = std::equal(h.begin(), h.begin() + ne, ref_fwd->begin());
+    float ti16 = time_launches<GV<V>>(reps, run_inv_w<V, 16>, B);
+    std::vector<uint64_t> h3(ne);
+    CK(cudaMemcpy(h3.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
+    printf("{\"variant\": %d, \"k_cols_fwd2_W16_ms\": %.4f, \"k_cols_inv2_W16_ms\": %.4f, \"match_fwd\": %d, \"match_inv\": %d}\n", V, tf16, ti16,
+           (int)okf16, (int)(h3 == *ref_inv));
+  }
   float tv = time_launches<GV<V>>(reps, run_inv_vec<V>, B);
   CK(cudaMemcpy(h.data(), B.out, ne * 8, cudaMemcpyDeviceToHost));
   const bool okv = *ref_inv == h;
@@ -271,7 +307,7 @@ int main(int argc, char** argv) {
   for (int round = 0; round < 2; ++round) {   // two rounds: A B A B
     bench<0>("round-1 reduce", reps, B, &rb, &rf, &ri);
     bench<1>("wide-eps reduce", reps, B, &rb, &rf, &ri);
-    bench<5>("wide-eps reduce + add_c correction as IMAD.WIDE", reps, B, &rb, &rf, &ri);
+
 
   }
   return 0;
