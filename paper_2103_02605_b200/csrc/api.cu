@@ -14,6 +14,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fcirc.h"
 #include "apps.cuh"
 #include "fcirc_kernels.cuh"
@@ -23,6 +25,16 @@
 namespace fcirc {
 
 static thread_local int64_t g_launches = 0;
+
+// NVTX ranges (SURVEY §5 tracing): one range per C-ABI call and, while kernel profiling is enabled,
+// one per kernel launch (named by kind), so nsys / ncu --nvtx timelines show the pass structure.
+// Header-only NVTX v3: a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+static const char* const kKindName[] = {"k_block fused", "k_block sub-problems", "k_cols forward", "k_cols inverse",
+                                        "application kernels"};
 
 // ------------------------------------------------------------------------------------------
 // optional per-launch event timing (fcirc_profile_enable / fcirc_profile_read)
@@ -43,6 +55,7 @@ static cudaEvent_t prof_event() {
 }
 void prof_begin(int kind, cudaStream_t st) {
   if (!g_prof_on) return;
+  nvtxRangePushA(kind >= 0 && kind < 5 ? kKindName[kind] : "kernel");
   std::lock_guard<std::mutex> lk(g_prof_mu);
   t_prof_kind = kind;
   t_prof_e0 = prof_event();
@@ -50,6 +63,7 @@ void prof_begin(int kind, cudaStream_t st) {
 }
 void prof_end(cudaStream_t st) {
   if (!g_prof_on || t_prof_kind < 0) return;
+  nvtxRangePop();
   std::lock_guard<std::mutex> lk(g_prof_mu);
   cudaEvent_t e1 = prof_event();
   cudaEventRecord(e1, st);
@@ -535,6 +549,7 @@ extern "C" {
 
 int bigint_mul(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t ny, uint32_t* z, int64_t batch,
                void* stream) {
+  NvtxRange nvtx_range("bigint_mul");
   g_launches = 0;
   if (!x || !y || !z || nx < 1 || ny < 1 || batch < 1) return FCIRC_EINVAL;
   if (overlaps(z, (size_t)((nx + ny) * batch) * 4, x, (size_t)(nx * batch) * 4) ||
@@ -545,12 +560,14 @@ int bigint_mul(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t ny, uin
 
 int fcirc_matvec(uint64_t p, uint64_t f, const void* a, const void* b, void* c, int64_t n, int64_t batch,
                  void* stream) {
+  NvtxRange nvtx_range("fcirc_matvec");
   g_launches = 0;
   return matvec_impl(p, f, a, b, c, n, batch, (cudaStream_t)stream);
 }
 
 int fcirc_circulant_matvec(uint64_t p, const void* a, const void* b, void* c, int64_t n, int64_t batch,
                            void* stream) {
+  NvtxRange nvtx_range("fcirc_circulant_matvec");
   g_launches = 0;
   if (!a || !b || !c || n < 1 || batch < 1) return FCIRC_EINVAL;
   const PrimeInfo* pi = prime_info(p);
@@ -577,6 +594,7 @@ int fcirc_circulant_matvec(uint64_t p, const void* a, const void* b, void* c, in
 
 int fcirc_matvec_host(uint64_t p, uint64_t f, const void* a, const void* b, void* c, int64_t n,
                       int64_t batch) {
+  NvtxRange nvtx_range("fcirc_matvec_host");
   g_launches = 0;
   if (!a || !b || !c || n < 1 || batch < 1) return FCIRC_EINVAL;
   const PrimeInfo* pi = prime_info(p);
@@ -593,6 +611,7 @@ int fcirc_matvec_host(uint64_t p, uint64_t f, const void* a, const void* b, void
 
 int fcirc_polymul(uint64_t p, const void* a, int64_t na, const void* b, int64_t nb, void* c, int64_t batch,
                   void* stream) {
+  NvtxRange nvtx_range("fcirc_polymul");
   g_launches = 0;
   if (!a || !b || !c || na < 1 || nb < 1 || batch < 1) return FCIRC_EINVAL;
   const PrimeInfo* pi = prime_info(p);
