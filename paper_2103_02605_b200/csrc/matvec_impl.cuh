@@ -164,7 +164,11 @@ static int launch_block(const F& fld, const BlockKArgs<F>& args, cudaStream_t st
     bool one_prime_per_cta = true;   // multi-prime: a staged CTA's IPC instances inside one prime
     if constexpr (kMulti<F>)
       one_prime_per_cta = args.mp.per % ipcsel<RR>(M) == 0 && args.mp.inst0 % ipcsel<RR>(M) == 0;
-    if ((args.k > 0 || args.units <= 64) && one_prime_per_cta)
+    // sub-problem launches read their twiddles through L1 / L2 (R = 16 at 1024 threads/SM): measured
+    // faster than staging them (512 threads/SM) once R = 16 won (profiles/r02l_ab_tma_stage.txt);
+    // FCIRC_U32_STAGE=1 restores the staged kernel
+    static const int stage = knob("U32_STAGE", 0);
+    if ((args.k > 0 || args.units <= 64) && one_prime_per_cta && (stage || args.k == 0))
       return launch_block_t<F, M, RR, false, true>(fld, args, st);
   }
   return launch_block_t<F, M, RR, EMB, false>(fld, args, st);
@@ -375,9 +379,12 @@ static int launch_cols_r(const F& fld, const ColKArgs<F>& args, int64_t inst, cu
     return launch_cols<F, K, INV, 16, true>(fld, args, inst, st);
   }
   static const int use_inv2 = knob("INV2", 1);
+  // depth from which the inverse column pass takes the TMA pipeline (FCIRC_TMA_MIN_K; instantiated
+  // from K = 7 on so the boundary can be re-swept without a rebuild)
+  static const int tma_min_k = knob("TMA_MIN_K", FTraits<F>::TMA_MIN_K);
   if constexpr (INV && K >= 6 && K <= 10) {
     // two column groups per thread below the TMA depth (and whenever FCIRC_TMA=0)
-    if (use_inv2 && (!use_tma || K < FTraits<F>::TMA_MIN_K) && args.m >= 2 * wsel<16>(K)) {
+    if (use_inv2 && (!use_tma || K < tma_min_k) && args.m >= 2 * wsel<16>(K)) {
       if (r == 8) return launch_cols_inv2<F, K, 8>(fld, args, inst, st);
       return launch_cols_inv2<F, K, 16>(fld, args, inst, st);
     }
@@ -385,9 +392,9 @@ static int launch_cols_r(const F& fld, const ColKArgs<F>& args, int64_t inst, cu
   // TMA pipeline when two stages + the exchange buffer fit in shared memory and the tensor-map bases
   // are 16-byte aligned (cuTensorMapEncodeTiled's requirement; an offset view of a caller's tensor
   // may be only element-aligned and then takes the plain column kernels below)
-  if constexpr (K >= FTraits<F>::TMA_MIN_K && 3 * (1 << K) * wsel<16>(K) * sizeof(E) <= 200 * 1024) {
+  if constexpr (K >= 7 && 3 * (1 << K) * wsel<16>(K) * sizeof(E) <= 200 * 1024) {
     const bool aligned = ((uintptr_t)args.src0 & 15) == 0 && (INV || ((uintptr_t)args.src1 & 15) == 0);
-    if (use_tma && aligned) {
+    if (use_tma && aligned && K >= tma_min_k) {
       if constexpr (K <= 10)
         if (r == 8) return launch_cols_tma<F, K, INV, 8>(fld, args, inst, st);
       return launch_cols_tma<F, K, INV, 16>(fld, args, inst, st);
