@@ -529,13 +529,15 @@ static int bigint_impl(const uint32_t* x, int64_t nx, const uint32_t* y, int64_t
   g.c123 = (uint32_t)invmod(mulmod(P1 % P3, P2 % P3, P3), P3);
   g.c123q = (uint32_t)(((uint64_t)g.c123 << 32) / P3);
   prof_begin(4, st);
-  k_crt_digits<<<(unsigned)(batch * nseg), kCarryThreads, 0, st>>>(r1, r2, r3, L, ncoef, nd, nseg, g, E, S);
+  launch_k(k_crt_digits, (unsigned)(batch * nseg), kCarryThreads, 0, st, (const uint32_t*)r1, (const uint32_t*)r2,
+           (const uint32_t*)r3, (int64_t)L, (int64_t)ncoef, (int64_t)nd, (int64_t)nseg, g, E, S);
   prof_end(st);
   prof_begin(4, st);
-  k_carry_top<<<(unsigned)batch, kTopThreads, 0, st>>>(S, nseg);
+  launch_k(k_carry_top, (unsigned)batch, kTopThreads, 0, st, S, (int64_t)nseg);
   prof_end(st);
   prof_begin(4, st);
-  k_carry_apply<<<(unsigned)(batch * nseg), kCarryThreads, 0, st>>>(E, nd, nseg, S, z, nx + ny);
+  launch_k(k_carry_apply, (unsigned)(batch * nseg), kCarryThreads, 0, st, (const uint32_t*)E, (int64_t)nd, (int64_t)nseg,
+           (const uint32_t*)S, z, (int64_t)(nx + ny));
   prof_end(st);
   g_launches += 3;   // k_crt_digits, k_carry_top, k_carry_apply
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;

@@ -8,6 +8,8 @@
 #pragma once
 #include <cstdint>
 
+#include "modarith.cuh"
+
 namespace fcirc {
 
 struct GarnerConsts {
@@ -117,6 +119,7 @@ __global__ void __launch_bounds__(kCarryThreads)
 k_crt_digits(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2, const uint32_t* __restrict__ r3,
              int64_t L, int64_t ncoef, int64_t nd, int64_t nseg, GarnerConsts g, uint32_t* __restrict__ E,
              uint32_t* __restrict__ seg_gp) {
+  pdl_entry();
   constexpr int NV = kCarryPer + kHalo;   // V_{j0 - kHalo + q}, q < NV
   const int64_t inst = blockIdx.x / nseg, sg = blockIdx.x - inst * nseg;
   const int64_t j0 = sg * kCarrySeg + (int64_t)threadIdx.x * kCarryPer;
@@ -219,6 +222,7 @@ k_crt_digits(const uint32_t* __restrict__ r1, const uint32_t* __restrict__ r2, c
 // one-warp loop serialised a global-load round trip per 32 segments).
 constexpr int kTopThreads = 1024;
 __global__ void __launch_bounds__(kTopThreads) k_carry_top(uint32_t* __restrict__ seg_gp, int64_t nseg) {
+  pdl_entry();
   uint32_t* s = seg_gp + (int64_t)blockIdx.x * nseg;
   const int64_t per = (nseg + kTopThreads - 1) / kTopThreads;
   const int64_t b0 = (int64_t)threadIdx.x * per, b1 = b0 + per < nseg ? b0 + per : nseg;
@@ -237,6 +241,7 @@ __global__ void __launch_bounds__(kTopThreads) k_carry_top(uint32_t* __restrict_
 __global__ void __launch_bounds__(kCarryThreads)
 k_carry_apply(const uint32_t* __restrict__ E, int64_t nd, int64_t nseg, const uint32_t* __restrict__ seg_cin,
               uint32_t* __restrict__ z, int64_t nw) {
+  pdl_entry();
   const int64_t inst = blockIdx.x / nseg, sg = blockIdx.x - inst * nseg;
   const int64_t j0 = sg * kCarrySeg + (int64_t)threadIdx.x * kCarryPer;
   uint32_t e[kCarryPer];

@@ -353,6 +353,7 @@ template <int M> struct TwStage<FieldU32M, M> { static constexpr bool value = M 
 template <class F, int M, int R, int IPC, int MINB = 1, bool EMB = false, bool TWS = false, bool SHF = false>
 __global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
 k_block(F fld0, BlockKArgs<F> args) {
+  pdl_entry();
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<M, R>;
@@ -572,6 +573,7 @@ __device__ __forceinline__ void col_inverse(T (&x)[R], T (*y)[R], T* bx, T* by, 
 template <class F, int K, int R, int W, bool INV, int MINB = 1, bool EMB = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols(F fld0, ColKArgs<F> args) {
+  pdl_entry();
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<K, R>;
@@ -629,6 +631,7 @@ k_cols(F fld0, ColKArgs<F> args) {
 template <class F, int K, int R, int W, int MINB = 1, bool EMB = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols_fwd2(F fld0, ColKArgs<F> args) {
+  pdl_entry();
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<K, R>;
@@ -699,6 +702,7 @@ template <> struct Vec2<uint64_t> { using type = ulonglong2; };
 template <class F, int K, int R, int W, int MINB = 1, bool EMB = false, bool VEC = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols_inv2(F fld0, ColKArgs<F> args) {
+  pdl_entry();
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<K, R>;
@@ -803,6 +807,7 @@ template <class F, int K, int R, int W, bool INV, int MINB = 1>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols_tma(F fld0, ColKArgs<F> args, const __grid_constant__ CUtensorMap map0, const __grid_constant__ CUtensorMap map1,
            int64_t ntiles) {
+  pdl_entry();
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<K, R>;
@@ -912,6 +917,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 template <class F, int M, int R>
 __global__ void __launch_bounds__(2 * (1 << M) / R, 1)
 k_block_pipe(F fld0, BlockKArgs<F> args) {
+  pdl_entry();
   using T = typename F::T;
   using Tw = typename F::Tw;
   using PH = Phases<M, R>;

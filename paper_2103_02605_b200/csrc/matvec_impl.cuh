@@ -86,7 +86,7 @@ static int launch_block_pipe(const F& fld, const BlockKArgs<F>& args, cudaStream
   a2.seq = seq;
   const int64_t grid = ((batch + 2 * seq - 1) / (2 * seq)) << args.k;
   prof_begin(1, st);
-  kern<<<(unsigned)grid, 2 * T, smem, st>>>(fld, a2);
+  launch_k(kern, (unsigned)grid, 2 * T, smem, st, fld, a2);
   prof_end(st);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
@@ -149,7 +149,7 @@ static int launch_block_t(const F& fld, const BlockKArgs<F>& args, cudaStream_t 
   const int64_t per_cta = (int64_t)IPC * a2.seq;
   const int64_t grid = ((batch + per_cta - 1) / per_cta) << args.k;
   prof_begin(args.k == 0 ? 0 : 1, st);
-  kern<<<(unsigned)grid, T * IPC, smem, st>>>(fld, a2);
+  launch_k(kern, (unsigned)grid, T * IPC, smem, st, fld, a2);
   prof_end(st);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
@@ -188,7 +188,7 @@ static int launch_cols(const F& fld, ColKArgs<F> args, int64_t instances, cudaSt
   args.units = instances * args.colblocks;
   dim3 grid((unsigned)args.units, INV ? 1 : 2);
   prof_begin(INV ? 3 : 2, st);
-  kern<<<grid, threads, smem, st>>>(fld, args);
+  launch_k(kern, grid, threads, smem, st, fld, args);
   prof_end(st);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
@@ -211,7 +211,7 @@ static int launch_cols_fwd2(const F& fld, ColKArgs<F> args, int64_t instances, c
   args.colblocks = args.m / W;
   args.units = instances * args.colblocks;
   prof_begin(2, st);
-  kern<<<(unsigned)args.units, threads, smem, st>>>(fld, args);
+  launch_k(kern, (unsigned)args.units, threads, smem, st, fld, args);
   prof_end(st);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
@@ -243,7 +243,7 @@ static int launch_cols_inv2(const F& fld, ColKArgs<F> args, int64_t instances, c
   args.colblocks = args.m / (2 * W);
   args.units = instances * args.colblocks;
   prof_begin(3, st);
-  kern<<<(unsigned)args.units, threads, smem, st>>>(fld, args);
+  launch_k(kern, (unsigned)args.units, threads, smem, st, fld, args);
   prof_end(st);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
@@ -303,7 +303,7 @@ static int launch_cols_tma(const F& fld, ColKArgs<F> args, int64_t instances, cu
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * occ);
   prof_begin(INV ? 3 : 2, st);
-  kern<<<(unsigned)grid, threads, smem, st>>>(fld, args, m0, m1, ntiles);
+  launch_k(kern, (unsigned)grid, threads, smem, st, fld, args, m0, m1, ntiles);
   prof_end(st);
   count_launch();
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;

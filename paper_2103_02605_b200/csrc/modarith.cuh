@@ -26,6 +26,16 @@
 
 namespace fcirc {
 
+// Programmatic dependent launch (PDL; launch attribute set unless FCIRC_PDL=0): every kernel of the path starts by
+// waiting for the previous kernel in the stream to complete (griddepcontrol.wait: all of its memory
+// visible) and then allows the next one to be scheduled (griddepcontrol.launch_dependents), so the
+// next kernel's CTAs fill the SMs freed during this kernel's last wave instead of waiting for a new
+// launch.  Both are no-ops for launches without the PDL attribute.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ------------------------------------------------------------------------------------------
 // 32-bit NTT primes
 // ------------------------------------------------------------------------------------------

@@ -47,6 +47,30 @@ inline bool smem_optin(const void* fn, size_t smem, std::atomic<uint32_t>& mask)
   return true;
 }
 
+// integer tuning knob read once from the environment (FCIRC_<name>), else `dflt` (api.cu)
+int knob(const char* name, int dflt);
+
+// Launch a kernel of the path on `st`, with the programmatic-dependent-launch attribute when
+// FCIRC_PDL (default 1; the kernels call pdl_entry(), modarith.cuh).
+template <class... KArgs, class... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  static const int pdl = knob("PDL", 1);   // profiles/r02n_ab_pdl.txt: +0.3..4 %, default on
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // launch bookkeeping (api.cu): optional per-launch CUDA-event timing and the launch counter
 void prof_begin(int kind, cudaStream_t st);
 void prof_end(cudaStream_t st);
@@ -55,9 +79,6 @@ void count_launch();
 // stream-ordered device scratch from the default memory pool (api.cu); free with ws_free on the same stream
 int ws_alloc(int dev, cudaStream_t st, size_t bytes, void** out);
 void ws_free(void* p, cudaStream_t st);
-
-// integer tuning knob read once from the environment (FCIRC_<name>), else `dflt`
-int knob(const char* name, int dflt);
 
 // bytes of a' + b' intermediates per chunk of the multi-pass schedule (FCIRC_CHUNK_BYTES)
 size_t chunk_bytes();
