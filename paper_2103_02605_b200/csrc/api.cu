@@ -198,6 +198,7 @@ static int get_plan(int dev, uint64_t p, uint64_t f, int L, cudaStream_t st, std
   size_t bytes = 0;
   int rc = FCIRC_OK;
   std::vector<TwU32> hf, hi;
+  std::vector<uint64_t> mf, mi;   // (host staging stays alive until the synchronisation below)
   if (!pi->wide) {
     hf.resize(n);
     hi.resize(n);
@@ -207,6 +208,18 @@ static int get_plan(int dev, uint64_t p, uint64_t f, int L, cudaStream_t st, std
     if (!rc) rc = upload(&dp->twi, hi.data(), n * sizeof(TwU32), ps);
     dp->last_si32 = shoup_pair(dp->hp.last_si, p);
     dp->last_k32 = shoup_pair(dp->hp.K, p);
+  } else if (pi->kind == KIND_GOLD) {
+    // Montgomery form of every constant operand (FieldGold::mulm): s R mod p with R = 2^64,
+    // 2^64 mod p = 2^32 - 1.  The host plan (fcirc_plan_table) keeps the plain values.
+    const uint64_t R = 0xFFFFFFFFull;
+    mf.resize(n);
+    mi.resize(n);
+    for (size_t i = 0; i < n; ++i) { mf[i] = mulmod(dp->hp.s[i], R, p); mi[i] = mulmod(dp->hp.sinv[i], R, p); }
+    bytes = 2 * n * 8;
+    if (!rc) rc = upload(&dp->twf, mf.data(), n * 8, ps);
+    if (!rc) rc = upload(&dp->twi, mi.data(), n * 8, ps);
+    dp->last_si64 = mulmod(dp->hp.last_si, R, p);
+    dp->last_k64 = mulmod(dp->hp.K, R, p);
   } else {
     bytes = 2 * n * 8;
     if (!rc) rc = upload(&dp->twf, dp->hp.s.data(), n * 8, ps);

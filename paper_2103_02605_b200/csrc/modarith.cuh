@@ -10,8 +10,9 @@
 //      var x var    : Montgomery REDC with R = 2^32, out [0,2p) (leaves only)
 //      lazy ranges  : forward butterflies keep values in [0,4p), inverse ones in [0,2p)
 //  * FieldGold: p = 2^64 - 2^32 + 1.  Values are kept "weakly reduced" in [0, 2^64).
-//      64x64 -> 128 with IMAD.WIDE chains, then the special reduction
-//      2^64 == 2^32 - 1 (=: EPS), 2^96 == -1 (mod p); no division, no table.
+//      64x64 -> 128 with IMAD.WIDE chains; const x var (twiddles, stored times 2^64 mod p) by a
+//      Montgomery reduction with R = 2^64 (8 add/sub, p^-1 = 1 + 2^32 mod 2^64); var x var
+//      (leaves) by the special reduction 2^64 == 2^32 - 1 (=: EPS), 2^96 == -1 (mod p).
 //
 // The in-place form of Algorithm 1 used by the kernels:
 //   forward (row a)   : (x, y) -> (x + s y, x - s y)      [rows of A_M1 and A_M2, P:66-67]
@@ -206,24 +207,56 @@ struct FieldGold {
         : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
     return mk(r0, r1);
   }
-  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b.
+  // 64 x 64 -> 128 -> canonical residue in [0, p), for any 64-bit a, b (the leaves: var x var).
   __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
     // ptxas expands mul.lo.u64 / mul.hi.u64 into IMAD.WIDE.U32 chains with carry predicates
     const uint64_t lo = a * b, hi = __umul64hi(a, b);
     return reduce4(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
   }
+  // Montgomery reduction with R = 2^64 (round 3 of the arithmetic): T 2^-64 mod p, canonical, for
+  // T = (t3:t2:t1:t0) with xh = (t3:t2) <= p - 2, i.e. for every product x * s with x < 2^64 and
+  // s < p (T <= (2^64 - 1)(p - 1) < (p - 1) 2^64).
+  //   p^-1 mod 2^64 = 1 + 2^32, so m = xl p^-1 mod 2^64 = (t0, a1) with a1 = t0 + t1 (mod 2^32),
+  //   e = carry of t0 + t1; (T - m p) / 2^64 = xh - (m - a1 - e) = (xh + a1 + e) - m, a value in
+  //   (-p, p) (m p <= (2^64 - 1) p and m p == xl mod 2^64); xh + a1 + e <= p - 2 + 2^32 < 2^64 (no
+  //   overflow); a borrow means the value is negative and adding p = subtracting EPS mod 2^64.
+  // Eight 32-bit add/sub with carry and no multiply (reduce4: one IMAD.WIDE + 13), and the result
+  // needs no canonicalisation.  The twist-table entries and scaling constants are stored times
+  // R mod p (= EPS) so that mulm(x, s R) = x s (api.cu: Montgomery form of the Goldilocks plan).
+  __device__ __forceinline__ static uint64_t mont_reduce(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 a1, x0, x1, m;\n\t"
+        "add.cc.u32  a1, %3, %2;\n\t"     // a1 = t0 + t1, CF = e
+        "addc.cc.u32 x0, %4, a1;\n\t"     // x = xh + a1 + e
+        "addc.u32    x1, %5, 0;\n\t"
+        "sub.cc.u32  %0, x0, %2;\n\t"     // r = x - m, m = (t0, a1)
+        "subc.cc.u32 %1, x1, a1;\n\t"
+        "subc.u32    m, 0, 0;\n\t"        // m = -borrow
+        "sub.cc.u32  %0, %0, m;\n\t"      // on a borrow: r - EPS = r + p (mod 2^64)
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+    return mk(r0, r1);
+  }
+  // x * s mod p, canonical, for any 64-bit x and a table constant sR = s R mod p (< p)
+  __device__ __forceinline__ static uint64_t mulm(uint64_t x, uint64_t sR) {
+    const uint64_t lo = x * sR, hi = __umul64hi(x, sR);
+    return mont_reduce(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
   __device__ __forceinline__ static uint64_t canon(uint64_t x) { return x >= P ? x - P : x; }
 
+  // Butterflies: every twiddle / scaling operand is a table constant in Montgomery form (mulm);
+  // the leaves multiply two variables (mul, plain reduction).
   // forward a: inputs weak; t = s y canonical -> single corrections
   __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
-    const uint64_t t = mul(y, s);
+    const uint64_t t = mulm(y, s);
     const uint64_t X = x;
     x = add_c(X, t);
     y = sub_c(X, t);
   }
   // forward b: t = s x canonical; t + y single correction; t - y with weak y needs two
   __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
-    const uint64_t t = mul(x, s);
+    const uint64_t t = mulm(x, s);
     const uint64_t Y = y;
     x = add_c(Y, t);
     y = sub_w(t, Y);
@@ -233,18 +266,18 @@ struct FieldGold {
   __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
     const uint64_t s = add_c(u, v);   // u + v < 2p: one correction, result weak
     const uint64_t d = sub_c(u, v);   // canonical
-    u = mul(s, si);
+    u = mulm(s, si);
     v = d;
   }
   __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
     const uint64_t s = add_c(u, v);
     const uint64_t d = sub_c(u, v);
-    u = mul(s, si_k);
-    v = mul(d, k);
+    u = mulm(s, si_k);
+    v = mulm(d, k);
   }
   __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
   __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
-    return mul(mul(a, b), k);
+    return mulm(mul(a, b), k);
   }
 };
 

@@ -76,3 +76,32 @@ def test_reduce4_canonical(seed, fn):
         v = t0 | (t1 << 32) | (t2 << 64) | (t3 << 96)
         r = f(t0, t1, t2, t3)
         assert r == v % P, (hex(v), hex(r))
+
+
+@pytest.mark.parametrize("seed", [6, 7])
+def test_mont_reduce_const_times_var(seed):
+    """FieldGold::mont_reduce (const x var, Montgomery R = 2^64): for T = x * s with any 64-bit x and
+    s < p it returns T * 2^-64 mod p, canonical (the kernels store every table constant as s R)."""
+    f = sim.helper(SRC, "mont_reduce")
+    rng = random.Random(seed)
+    rinv = pow(1 << 64, -1, P)
+    xs = EDGE + [rng.getrandbits(64) for _ in range(1500)] + [M64 - rng.getrandbits(33) for _ in range(500)]
+    ss = [0, 1, 2, P - 1, P - 2, 0xFFFFFFFF, 1 << 32, (1 << 32) + 1, 0x8000000000000000, 0xFFFFFFFF00000000,
+          (1 << 32) - 1 + (1 << 63)] + [rng.randrange(P) for _ in range(40)] + [P - 1 - rng.getrandbits(33) for _ in range(20)]
+    for x in xs:
+        for s in ss:
+            t = x * s
+            r = f(*[(t >> (32 * i)) & 0xFFFFFFFF for i in range(4)])
+            assert r == t * rinv % P, (hex(x), hex(s), hex(r))
+
+
+def test_mont_reduce_precondition_boundary():
+    """The largest high word the reduction admits is p - 2 (x = 2^64 - 1, s = p - 1): still exact."""
+    f = sim.helper(SRC, "mont_reduce")
+    rinv = pow(1 << 64, -1, P)
+    for x in [M64, M64 - 1, P, P - 1]:
+        for s in [P - 1, P - 2]:
+            t = x * s
+            assert (t >> 64) <= P - 2
+            r = f(*[(t >> (32 * i)) & 0xFFFFFFFF for i in range(4)])
+            assert r == t * rinv % P

@@ -132,9 +132,10 @@ def run(text: str, nout: int, inputs):
 
 
 def helper(src: str, fn: str):
-    """Python callable on 64-bit values for FieldGold.<fn> (add_c, sub_c, sub_w) or reduce4."""
+    """Python callable on 64-bit values for FieldGold.<fn> (add_c, sub_c, sub_w) or on the four
+    product words for the reductions (reduce4, mont_reduce)."""
     text, nout, nin = extract(src, fn)
-    if fn.startswith("reduce4"):
+    if fn.startswith("reduce4") or fn == "mont_reduce":
         def f(t0, t1, t2, t3):
             r0, r1 = run(text, nout, [t0, t1, t2, t3])
             return r0 | (r1 << 32)
