@@ -23,122 +23,37 @@ namespace fcirc {
 
 template <int V>
 struct GV : FieldGold {
-  // reduce variants
-  __device__ __forceinline__ static uint64_t red(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
-    if constexpr (V == 0 || V == 4) {
-      return reduce4(t0, t1, t2, t3);
-    } else if constexpr (V == 2) {
-      uint32_t r0, r1;
-      // V2: V1's WIDE EPS product, canonicalisation as r + EPS with carry -> select
-      asm("{\n\t.reg .u32 c, m, h, s0, s1;\n\t.reg .u64 T, E, R;\n\t.reg .pred p;\n\t"
-          "mov.b64 T, {%2, %3};\n\t"
-          "mul.wide.u32 E, %4, 0xffffffff;\n\t"
-          "add.cc.u64 R, T, E;\n\t"
-          "addc.u32 c, 0, 0;\n\t"
-          "mov.b64 {%0, %1}, R;\n\t"
-          "sub.cc.u32      %0, %0, %5;\n\t"
-          "subc.cc.u32     %1, %1, 0;\n\t"
-          "subc.u32        c, c, 0;\n\t"
-          "neg.s32         m, c;\n\t"
-          "shr.s32         h, c, 31;\n\t"
-          "add.cc.u32      %0, %0, m;\n\t"
-          "addc.u32        %1, %1, h;\n\t"
-          "add.cc.u32      s0, %0, 0xffffffff;\n\t"
-          "addc.cc.u32     s1, %1, 0;\n\t"
-          "addc.u32        c, 0, 0;\n\t"
-          "setp.ne.u32     p, c, 0;\n\t"
-          "selp.b32        %0, s0, %0, p;\n\t"
-          "selp.b32        %1, s1, %1, p;\n\t"
-          "}"
-          : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
-      return mk(r0, r1);
-    } else {
-      uint32_t r0, r1;
-      // V >= 1: t2 * EPS + (t1:t0) as one IMAD.WIDE.U32 with carry out (mul.wide + add.cc.u64)
-      asm("{\n\t.reg .u32 c, m, h;\n\t.reg .u64 T, E, R;\n\t.reg .pred p, q;\n\t"
-          "mov.b64 T, {%2, %3};\n\t"
-          "mul.wide.u32 E, %4, 0xffffffff;\n\t"
-          "add.cc.u64 R, T, E;\n\t"
-          "addc.u32 c, 0, 0;\n\t"
-          "mov.b64 {%0, %1}, R;\n\t"
-          "sub.cc.u32      %0, %0, %5;\n\t"
-          "subc.cc.u32     %1, %1, 0;\n\t"
-          "subc.u32        c, c, 0;\n\t"
-          "neg.s32         m, c;\n\t"
-          "shr.s32         h, c, 31;\n\t"
-          "add.cc.u32      %0, %0, m;\n\t"
-          "addc.u32        %1, %1, h;\n\t"
-          "setp.eq.u32     p, %1, 0xffffffff;\n\t"
-          "setp.ne.and.u32 q, %0, 0, p;\n\t"
-          "@q sub.u32      %0, %0, 1;\n\t"
-          "@q mov.u32      %1, 0;\n\t"
-          "}"
-          : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
-      return mk(r0, r1);
-    }
+  // add_c with the carry correction as plain adds (lo - c with borrow, hi + c - borrow: 4 ALU adds +
+  // the carry materialisation) instead of ISETP + two predicated VIADD (FMA-heavy pipe)
+  __device__ __forceinline__ static uint64_t add_ca(uint64_t a, uint64_t b) {
+    uint32_t s0, s1;
+    asm("{\n\t.reg .u32 c, h;\n\t"
+        "add.cc.u32  %0, %2, %4;\n\t"
+        "addc.cc.u32 %1, %3, %5;\n\t"
+        "addc.u32    c, 0, 0;\n\t"
+        "add.u32     h, %1, c;\n\t"
+        "sub.cc.u32  %0, %0, c;\n\t"
+        "subc.u32    %1, h, 0;\n\t"
+        "}"
+        : "=&r"(s0), "=&r"(s1) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
+    return mk(s0, s1);
   }
-  // V >= 3: the 64 x 64 product as four mul.wide.u32 partials with explicit carry chains (ptxas then
-  // emits 4 IMAD.WIDE.U32 + 4 carry instructions; the C-level lo/hi form sometimes recomputes a0 b0)
-  __device__ __forceinline__ static void prod(uint64_t a, uint64_t b, uint32_t& t0, uint32_t& t1, uint32_t& t2,
-                                              uint32_t& t3) {
-    asm("{\n\t.reg .u32 a0, a1, b0, b1, l1, c0, c1, h0, h1, k;\n\t.reg .u64 L, X, Y, H;\n\t"
-        "mov.b64 {a0, a1}, %4;\n\t"
-        "mov.b64 {b0, b1}, %5;\n\t"
-        "mul.wide.u32 L, a0, b0;\n\t"
-        "mul.wide.u32 X, a0, b1;\n\t"
-        "mul.wide.u32 Y, a1, b0;\n\t"
-        "add.cc.u64 X, X, Y;\n\t"
-        "addc.u32 k, 0, 0;\n\t"
-        "mul.wide.u32 H, a1, b1;\n\t"
-        "mov.b64 {%0, l1}, L;\n\t"
-        "mov.b64 {c0, c1}, X;\n\t"
-        "mov.b64 {h0, h1}, H;\n\t"
-        "add.cc.u32 %1, l1, c0;\n\t"
-        "addc.cc.u32 %2, h0, c1;\n\t"
-        "addc.u32 %3, h1, k;\n\t}"
-        : "=r"(t0), "=r"(t1), "=r"(t2), "=r"(t3) : "l"(a), "l"(b));
-  }
-  __device__ __forceinline__ static uint64_t mul(uint64_t a, uint64_t b) {
-    if constexpr (V >= 3) {
-      uint32_t t0, t1, t2, t3;
-      prod(a, b, t0, t1, t2, t3);
-      return red(t0, t1, t2, t3);
-    }
-    const uint64_t lo = a * b, hi = __umul64hi(a, b);
-    return red(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
-  }
-  // V == 5: a + b mod p with the carry correction +c*EPS as ONE IMAD.WIDE.U32 (c * 0xffffffff + s),
-  // moving it from the ALU pipe (ISETP + two predicated adds) to the FMA pipe
-  __device__ __forceinline__ static uint64_t addc_v(uint64_t a, uint64_t b) {
-    if constexpr (V == 5) {
-      uint64_t r;
-      asm("{\n\t.reg .u32 s0, s1, c;\n\t.reg .u64 S, E;\n\t"
-          "add.cc.u32  s0, %1, %3;\n\t"
-          "addc.cc.u32 s1, %2, %4;\n\t"
-          "addc.u32    c, 0, 0;\n\t"
-          "mov.b64     S, {s0, s1};\n\t"
-          "mul.wide.u32 E, c, 0xffffffff;\n\t"
-          "add.u64     %0, S, E;\n\t}"
-          : "=l"(r) : "r"(lo32(a)), "r"(hi32(a)), "r"(lo32(b)), "r"(hi32(b)));
-      return r;
-    } else {
-      return add_c(a, b);
-    }
-  }
+  // V1: arithmetic add_c in the inverse butterflies; V2: in fwd_b; V3: everywhere; V4: fwd_a
+  static constexpr bool A_FA = V == 3 || V == 4, A_FB = V == 2 || V == 3, A_INV = V == 1 || V == 3;
   __device__ __forceinline__ void fwd_a(uint64_t& x, uint64_t& y, uint64_t s) const {
-    const uint64_t t = mul(y, s); const uint64_t X = x; x = addc_v(X, t); y = sub_c(X, t);
+    const uint64_t t = mulm(y, s); const uint64_t X = x;
+    x = A_FA ? add_ca(X, t) : add_c(X, t); y = sub_c(X, t);
   }
   __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
-    const uint64_t t = mul(x, s); const uint64_t Y = y; x = addc_v(Y, t); y = sub_w(t, Y);
+    const uint64_t t = mulm(x, s); const uint64_t Y = y;
+    x = A_FB ? add_ca(Y, t) : add_c(Y, t); y = sub_w(t, Y);
   }
   __device__ __forceinline__ void inv(uint64_t& u, uint64_t& v, uint64_t si) const {
-    const uint64_t s = addc_v(u, v); const uint64_t d = sub_c(u, v); u = mul(s, si); v = d;
+    const uint64_t s = A_INV ? add_ca(u, v) : add_c(u, v); const uint64_t d = sub_c(u, v); u = mulm(s, si); v = d;
   }
   __device__ __forceinline__ void inv_last(uint64_t& u, uint64_t& v, uint64_t si_k, uint64_t k) const {
-    const uint64_t s = add_c(u, v); const uint64_t d = sub_c(u, v); u = mul(s, si_k); v = mul(d, k);
+    const uint64_t s = add_c(u, v); const uint64_t d = sub_c(u, v); u = mulm(s, si_k); v = mulm(d, k);
   }
-  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
-  __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const { return mul(mul(a, b), k); }
 };
 
 }  // namespace fcirc
@@ -305,8 +220,11 @@ int main(int argc, char** argv) {
   // opt-in smem for the fwd/inv kernels (32 KB: not needed) -- k_block needs 64 KB
   std::vector<uint64_t> rb, rf, ri;
   for (int round = 0; round < 2; ++round) {   // two rounds: A B A B
-    bench<0>("round-1 reduce", reps, B, &rb, &rf, &ri);
-    bench<1>("wide-eps reduce", reps, B, &rb, &rf, &ri);
+    bench<0>("library (Montgomery const x var)", reps, B, &rb, &rf, &ri);
+    bench<1>("arith add_c in inv", reps, B, &rb, &rf, &ri);
+    bench<2>("arith add_c in fwd_b", reps, B, &rb, &rf, &ri);
+    bench<3>("arith add_c everywhere", reps, B, &rb, &rf, &ri);
+    bench<4>("arith add_c in fwd_a", reps, B, &rb, &rf, &ri);
 
 
   }
