@@ -93,34 +93,41 @@ struct EmbedIO {
 };
 
 template <class T>
-__device__ __forceinline__ T limb_at(const T* w, int64_t m) {
-  if constexpr (sizeof(T) == 4) return (w[m >> 1] >> (16 * (m & 1))) & 0xFFFFu;
+__device__ __forceinline__ T limb_at(const T* w, uint32_t m) {
+  if constexpr (sizeof(T) == 4) return (__ldg(w + (m >> 1)) >> (16 * (m & 1))) & 0xFFFFu;
   else return 0;  // limbs are only used with the 32-bit primes
 }
-// element `pos` of the row (second = false) or the vector (second = true) of instance `inst`
-template <class T>
-__device__ __forceinline__ T io_load(const T* src, int64_t inst, int64_t pos, int64_t n, bool second, const EmbedIO& io) {
-  if (io.mode == EMB_PLAIN) return src[inst * n + pos];
-  if (io.mode == EMB_POLY) {
-    if (second) return pos < io.nb ? src[inst * io.nb + pos] : (T)0;
+// Element `pos` (< n <= 2^24) of the row (SECOND = false) or the vector (SECOND = true) of caller
+// instance `inst`, for the compile-time embedding MODE (the kernels are instantiated per mode: with a
+// run-time mode switch every embedded load carried all four index paths in 64-bit arithmetic, 3x the
+// SASS of the plain column pass).  Zero padding is never read.
+template <int MODE, bool SECOND, class T>
+__device__ __forceinline__ T io_load(const T* src, int64_t inst, uint32_t pos, uint32_t n, const EmbedIO& io) {
+  if constexpr (MODE == EMB_PLAIN) {
+    return src[inst * n + pos];
+  } else if constexpr (MODE == EMB_POLY) {
+    const uint32_t na = (uint32_t)io.na, nb = (uint32_t)io.nb;
+    if constexpr (SECOND) return pos < nb ? src[inst * io.nb + pos] : (T)0;
     const T* ai = src + inst * io.na;
-    return pos == 0 ? ai[0] : (pos > n - io.na ? ai[n - pos] : (T)0);
-  }
-  if (io.mode == EMB_ANYN) {
-    if (second) return pos < io.nb ? src[inst * io.nb + pos] : (T)0;
+    return pos == 0 ? ai[0] : (pos > n - na ? ai[n - pos] : (T)0);
+  } else if constexpr (MODE == EMB_ANYN) {
+    const uint32_t na = (uint32_t)io.na, nb = (uint32_t)io.nb;
+    if constexpr (SECOND) return pos < nb ? src[inst * io.nb + pos] : (T)0;
     const T* ai = src + inst * io.na;
-    return pos < io.na ? ai[pos] : (pos > n - io.na ? ai[pos - (n - io.na)] : (T)0);
+    return pos < na ? ai[pos] : (pos > n - na ? ai[pos - (n - na)] : (T)0);
+  } else {   // EMB_LIMBS: na, nb are 32-bit words (2 limbs each)
+    const uint32_t la = 2 * (uint32_t)io.na, lb = 2 * (uint32_t)io.nb;
+    if constexpr (SECOND) return pos < lb ? limb_at(src + inst * io.nb, pos) : (T)0;
+    const T* xi = src + inst * io.na;
+    return pos == 0 ? limb_at(xi, 0u) : (pos > n - la ? limb_at(xi, n - pos) : (T)0);
   }
-  if (second) return pos < 2 * io.nb ? limb_at(src + inst * io.nb, pos) : (T)0;
-  const T* xi = src + inst * io.na;
-  return pos == 0 ? limb_at(xi, 0) : (pos > n - 2 * io.na ? limb_at(xi, n - pos) : (T)0);
 }
-template <class T>
-__device__ __forceinline__ void io_store(T* dst, int64_t inst, int64_t pos, int64_t n, T v, const EmbedIO& io) {
-  if (emb_truncates(io.mode)) {
-    if (pos < io.nc) dst[inst * io.nc + pos] = v;
+template <int MODE, class T>
+__device__ __forceinline__ void io_store(T* dst, int64_t inst, uint32_t pos, uint32_t n, T v, const EmbedIO& io) {
+  if constexpr (MODE == EMB_POLY || MODE == EMB_ANYN) {
+    if (pos < (uint32_t)io.nc) dst[inst * io.nc + pos] = v;
   } else {
-    dst[inst * n + pos] = v;
+    dst[inst * (int64_t)n + pos] = v;
   }
 }
 
@@ -350,7 +357,7 @@ template <class F, int M> struct TwStage { static constexpr bool value = false; 
 template <int M> struct TwStage<FieldU32, M> { static constexpr bool value = M >= 6; };
 template <int M> struct TwStage<FieldU32M, M> { static constexpr bool value = M >= 6; };
 
-template <class F, int M, int R, int IPC, int MINB = 1, bool EMB = false, bool TWS = false, bool SHF = false>
+template <class F, int M, int R, int IPC, int MINB = 1, int EMB = EMB_PLAIN, bool TWS = false, bool SHF = false>
 __global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
 k_block(F fld0, BlockKArgs<F> args) {
   pdl_entry();
@@ -428,8 +435,8 @@ k_block(F fld0, BlockKArgs<F> args) {
     for (int s = 0; s < R; ++s) {
       const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
       if constexpr (EMB) {
-        xa[s] = io_load(args.a, src_inst<F>(args, inst), ad, m, false, args.io);
-        xb[s] = io_load(args.b, src_inst<F>(args, inst), ad, m, true, args.io);
+        xa[s] = io_load<EMB, false>(args.a, src_inst<F>(args, inst), ad, m, args.io);
+        xb[s] = io_load<EMB, true>(args.b, src_inst<F>(args, inst), ad, m, args.io);
       } else {
         xa[s] = args.a[base + ad];
         xb[s] = args.b[base + ad];
@@ -466,7 +473,7 @@ k_block(F fld0, BlockKArgs<F> args) {
   if constexpr (M == 0) {
     if (active) {
       const T v = fld.single(xa[0], xb[0], view_lk<F>(fv, args));
-      if constexpr (EMB) io_store(args.out, inst, 0, 1, v, args.io);
+      if constexpr (EMB) io_store<EMB>(args.out, inst, 0, 1, v, args.io);
       else args.out[base] = v;
     }
   } else {
@@ -495,7 +502,7 @@ k_block(F fld0, BlockKArgs<F> args) {
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const int ad = PH::ins_t(0, t) + PH::cslot(0, s);
-        if constexpr (EMB) io_store(args.out, inst, ad, m, xm[s], args.io);
+        if constexpr (EMB) io_store<EMB>(args.out, inst, ad, m, xm[s], args.io);
         else args.out[base + ad] = xm[s];
       }
     }
@@ -570,7 +577,7 @@ __device__ __forceinline__ void col_inverse(T (&x)[R], T (*y)[R], T* bx, T* by, 
 }
 
 // k_cols: one operand per thread; the forward pass covers a (blockIdx.y = 0) and b (= 1)
-template <class F, int K, int R, int W, bool INV, int MINB = 1, bool EMB = false>
+template <class F, int K, int R, int W, bool INV, int MINB = 1, int EMB = EMB_PLAIN>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols(F fld0, ColKArgs<F> args) {
   pdl_entry();
@@ -599,7 +606,11 @@ k_cols(F fld0, ColKArgs<F> args) {
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     const int64_t row = PH::ins_t(ph_in, t) + PH::cslot(ph_in, s);
-    if constexpr (EMB && !INV) x[s] = io_load(src, src_inst<F>(args, inst), col + row * m, args.n, second, args.io);
+    if constexpr (EMB && !INV) {
+      const uint32_t pos = (uint32_t)(col + row * m);
+      x[s] = second ? io_load<EMB, true>(src, src_inst<F>(args, inst), pos, (uint32_t)args.n, args.io)
+                    : io_load<EMB, false>(src, src_inst<F>(args, inst), pos, (uint32_t)args.n, args.io);
+    }
     else x[s] = src[base + row * m];
   }
   if constexpr (!INV) {
@@ -617,7 +628,7 @@ k_cols(F fld0, ColKArgs<F> args) {
 #pragma unroll
   for (int s = 0; s < R; ++s) {
     const int64_t row = PH::ins_t(ph_out, t) + PH::cslot(ph_out, s);
-    if constexpr (EMB && INV) io_store(dst, inst, col + row * m, args.n, x[s], args.io);
+    if constexpr (EMB && INV) io_store<EMB>(dst, inst, (uint32_t)(col + row * m), (uint32_t)args.n, x[s], args.io);
     else dst[base + row * m] = x[s];
   }
 }
@@ -628,7 +639,7 @@ k_cols(F fld0, ColKArgs<F> args) {
 // the Goldilocks column pass needs to hide its carry-chain latency (profiles/r01e: k_cols<fwd>
 // stalled on "wait" at 2.3 per issue vs 1.2 in k_block).
 // ------------------------------------------------------------------------------------------
-template <class F, int K, int R, int W, int MINB = 1, bool EMB = false>
+template <class F, int K, int R, int W, int MINB = 1, int EMB = EMB_PLAIN>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols_fwd2(F fld0, ColKArgs<F> args) {
   pdl_entry();
@@ -659,8 +670,9 @@ k_cols_fwd2(F fld0, ColKArgs<F> args) {
   for (int s = 0; s < R; ++s) {
     const int64_t row = PH::ins_t(0, t) + PH::cslot(0, s);
     if constexpr (EMB) {
-      xa[s] = io_load(args.src0, src_inst<F>(args, inst), col + row * m, args.n, false, args.io);
-      xb[s] = io_load(args.src1, src_inst<F>(args, inst), col + row * m, args.n, true, args.io);
+      const uint32_t pos = (uint32_t)(col + row * m);
+      xa[s] = io_load<EMB, false>(args.src0, src_inst<F>(args, inst), pos, (uint32_t)args.n, args.io);
+      xb[s] = io_load<EMB, true>(args.src1, src_inst<F>(args, inst), pos, (uint32_t)args.n, args.io);
     } else if constexpr (OFF32) {
       xa[s] = pa[(uint32_t)row * mm];
       xb[s] = pb[(uint32_t)row * mm];
@@ -699,7 +711,7 @@ k_cols_fwd2(F fld0, ColKArgs<F> args) {
 template <class T> struct Vec2;
 template <> struct Vec2<uint32_t> { using type = uint2; };
 template <> struct Vec2<uint64_t> { using type = ulonglong2; };
-template <class F, int K, int R, int W, int MINB = 1, bool EMB = false, bool VEC = false>
+template <class F, int K, int R, int W, int MINB = 1, int EMB = EMB_PLAIN, bool VEC = false>
 __global__ void __launch_bounds__(W * ((1 << K) / R), MINB)
 k_cols_inv2(F fld0, ColKArgs<F> args) {
   pdl_entry();
@@ -749,8 +761,8 @@ k_cols_inv2(F fld0, ColKArgs<F> args) {
 #pragma unroll
     for (int s = 0; s < R; ++s) {
       const int64_t pos = col + (int64_t)(PH::ins_t(0, t) + PH::cslot(0, s)) * m;
-      io_store(args.dst0, inst, pos, args.n, xa[s], args.io);
-      io_store(args.dst0, inst, pos + W, args.n, xb[s], args.io);
+      io_store<EMB>(args.dst0, inst, (uint32_t)pos, (uint32_t)args.n, xa[s], args.io);
+      io_store<EMB>(args.dst0, inst, (uint32_t)(pos + W), (uint32_t)args.n, xb[s], args.io);
     }
   } else {
 #pragma unroll

@@ -92,7 +92,22 @@ static int launch_block_pipe(const F& fld, const BlockKArgs<F>& args, cudaStream
   return cudaPeekAtLastError() == cudaSuccess ? FCIRC_OK : FCIRC_ECUDA;
 }
 
-template <class F, int M, int RR, bool EMB, bool TWS>
+// An application call's embedding mode as a compile-time constant: the first / last pass kernels are
+// instantiated per mode (TRUNC: only the truncating modes, whose inverse pass stores through the
+// embedding; limbs only for the 32-bit fields).
+template <class F, bool TRUNC = false, class Fn>
+static int with_emb(int mode, Fn&& fn) {
+  switch (mode) {
+    case EMB_POLY: return fn(std::integral_constant<int, EMB_POLY>{});
+    case EMB_ANYN: return fn(std::integral_constant<int, EMB_ANYN>{});
+    case EMB_LIMBS:
+      if constexpr (!TRUNC && sizeof(typename F::T) == 4) return fn(std::integral_constant<int, EMB_LIMBS>{});
+      return FCIRC_EINVAL;
+    default: return FCIRC_EINVAL;
+  }
+}
+
+template <class F, int M, int RR, int EMB, bool TWS>
 static int launch_block_t(const F& fld, const BlockKArgs<F>& args, cudaStream_t st) {
   constexpr int R = rsel<RR>(M), IPC = ipcsel<RR>(M);
   constexpr int T = (1 << M) / R;
@@ -158,7 +173,7 @@ static int launch_block_t(const F& fld, const BlockKArgs<F>& args, cudaStream_t 
 // The 32-bit fields stage their twiddle slices in smem for sub-problem launches (k > 0), and for
 // fused launches of a small batch (latency-bound: one coalesced table load per CTA instead of a
 // dependent L2 round trip per phase); large fused batches share the table through L1/L2 instead.
-template <class F, int M, int RR, bool EMB = false>
+template <class F, int M, int RR, int EMB = EMB_PLAIN>
 static int launch_block(const F& fld, const BlockKArgs<F>& args, cudaStream_t st) {
   if constexpr (TwStage<F, M>::value && !EMB) {
     bool one_prime_per_cta = true;   // multi-prime: a staged CTA's IPC instances inside one prime
@@ -169,12 +184,12 @@ static int launch_block(const F& fld, const BlockKArgs<F>& args, cudaStream_t st
     // FCIRC_U32_STAGE=1 restores the staged kernel
     static const int stage = knob("U32_STAGE", 0);
     if ((args.k > 0 || args.units <= 64) && one_prime_per_cta && (stage || args.k == 0))
-      return launch_block_t<F, M, RR, false, true>(fld, args, st);
+      return launch_block_t<F, M, RR, EMB_PLAIN, true>(fld, args, st);
   }
   return launch_block_t<F, M, RR, EMB, false>(fld, args, st);
 }
 
-template <class F, int K, bool INV, int RR, bool EMB = false>
+template <class F, int K, bool INV, int RR, int EMB = EMB_PLAIN>
 static int launch_cols(const F& fld, ColKArgs<F> args, int64_t instances, cudaStream_t st) {
   constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
   constexpr int threads = W * ((1 << K) / R);
@@ -195,7 +210,7 @@ static int launch_cols(const F& fld, ColKArgs<F> args, int64_t instances, cudaSt
 }
 
 // dual forward column pass (a and b per thread)
-template <class F, int K, int RR, bool EMB = false>
+template <class F, int K, int RR, int EMB = EMB_PLAIN>
 static int launch_cols_fwd2(const F& fld, ColKArgs<F> args, int64_t instances, cudaStream_t st) {
   constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
   constexpr int threads = W * ((1 << K) / R);
@@ -218,7 +233,7 @@ static int launch_cols_fwd2(const F& fld, ColKArgs<F> args, int64_t instances, c
 }
 
 // inverse column pass, two column groups per thread (plain operands; needs m >= 2 W)
-template <class F, int K, int RR, bool EMB = false>
+template <class F, int K, int RR, int EMB = EMB_PLAIN>
 static int launch_cols_inv2(const F& fld, ColKArgs<F> args, int64_t instances, cudaStream_t st) {
   constexpr int R = rsel<RR>(K), W = wsel<RR>(K);
   constexpr int threads = W * ((1 << K) / R);
@@ -326,7 +341,8 @@ template <> struct RDefault<FieldM31x2> { static constexpr int RB = 8, RBF = 8, 
 template <class F, int M>
 static int launch_block_r(const F& fld, const BlockKArgs<F>& args, cudaStream_t st) {
   // the application embeddings (fused path only) use one variant: the default R
-  if (args.k == 0 && args.io.mode != EMB_PLAIN) return launch_block<F, M, RDefault<F>::RB, true>(fld, args, st);
+  if (args.k == 0 && args.io.mode != EMB_PLAIN)
+    return with_emb<F>(args.io.mode, [&](auto md) { return launch_block<F, M, RDefault<F>::RB, decltype(md)::value>(fld, args, st); });
   // latency-bound small fused batches (C1: one 1024-point product): 4 elements per thread, i.e.
   // more and shorter dependency chains (C1 7.5 -> 5.6 us per step, profiles/r01m_sweep_c1_small_r.txt)
   if constexpr (M >= 8 && M <= 10) {
@@ -363,7 +379,8 @@ static int launch_cols_r(const F& fld, const ColKArgs<F>& args, int64_t inst, cu
   using E = typename F::T;
   const int mode = args.io.mode;
   if constexpr (!INV && K >= 4 && K <= 10) {
-    if (use_fwd2 && mode != EMB_PLAIN) return launch_cols_fwd2<F, K, 16, true>(fld, args, inst, st);
+    if (use_fwd2 && mode != EMB_PLAIN)
+      return with_emb<F>(mode, [&](auto md) { return launch_cols_fwd2<F, K, 16, decltype(md)::value>(fld, args, inst, st); });
     if (use_fwd2 && mode == EMB_PLAIN && K >= 6) {
       if (r == 8) return launch_cols_fwd2<F, K, 8>(fld, args, inst, st);
       return launch_cols_fwd2<F, K, 16>(fld, args, inst, st);
@@ -372,11 +389,13 @@ static int launch_cols_r(const F& fld, const ColKArgs<F>& args, int64_t inst, cu
   // application embeddings: the forward pass reads embedded operands (above); the inverse pass of
   // a truncating embedding (polynomial, any-n) stores through EMB; a limb embedding's inverse
   // output is a plain [batch][n] array and takes the plain selection below
-  if (!INV && mode != EMB_PLAIN) return launch_cols<F, K, INV, 16, true>(fld, args, inst, st);
+  if (!INV && mode != EMB_PLAIN)
+    return with_emb<F>(mode, [&](auto md) { return launch_cols<F, K, INV, 16, decltype(md)::value>(fld, args, inst, st); });
   if (INV && emb_truncates(mode)) {
     if constexpr (K >= 6 && K <= 10)
-      if (args.m >= 2 * wsel<16>(K)) return launch_cols_inv2<F, K, 16, true>(fld, args, inst, st);
-    return launch_cols<F, K, INV, 16, true>(fld, args, inst, st);
+      if (args.m >= 2 * wsel<16>(K))
+        return with_emb<F, true>(mode, [&](auto md) { return launch_cols_inv2<F, K, 16, decltype(md)::value>(fld, args, inst, st); });
+    return with_emb<F, true>(mode, [&](auto md) { return launch_cols<F, K, INV, 16, decltype(md)::value>(fld, args, inst, st); });
   }
   static const int use_inv2 = knob("INV2", 1);
   // depth from which the inverse column pass takes the TMA pipeline (FCIRC_TMA_MIN_K; instantiated
