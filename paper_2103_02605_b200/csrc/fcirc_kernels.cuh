@@ -172,7 +172,7 @@ struct NoView {};
 template <class F, class A>
 __device__ __forceinline__ auto field_view(const F& fld, const A& args, int64_t inst) {
   if constexpr (kMulti<F>) {
-    const int64_t q = (args.mp.inst0 + inst) / args.mp.per;
+    const uint32_t q = (uint32_t)(args.mp.inst0 + inst) / (uint32_t)args.mp.per;   // < 2^31 instances
     const PrimeSel& ps = q == 0 ? args.mp.ps[0] : (q == 1 ? args.mp.ps[1] : args.mp.ps[2]);
     return FieldView<F>{F{ps.fld}, ps.twf, ps.twi, ps.last_si, ps.last_k};
   } else {
@@ -193,7 +193,7 @@ template <class F, class A> __device__ __forceinline__ typename F::Tw view_lk(co
 // the caller's instance whose operands instance `inst` of the launch reads
 template <class F, class A>
 __device__ __forceinline__ int64_t src_inst(const A& args, int64_t inst) {
-  if constexpr (kMulti<F>) return (args.mp.inst0 + inst) % args.mp.per;
+  if constexpr (kMulti<F>) return (uint32_t)(args.mp.inst0 + inst) % (uint32_t)args.mp.per;
   else return inst;
 }
 
@@ -534,6 +534,10 @@ struct ColArgs {
 // the prime table; every other field takes the plain struct (unchanged parameter block).
 template <class F> struct ColArgsM : ColArgs<F> { MultiPrime mp; };
 template <class F> using ColKArgs = typename std::conditional<kMulti<F>, ColArgsM<F>, ColArgs<F>>::type;
+// colblocks (= m / W or m / (2 W)) is a power of two: the block -> (instance, column block) split is a
+// shift and a mask instead of a 64-bit division per thread
+template <class A>
+__device__ __forceinline__ int cb_log(const A& args) { return __ffsll((long long)args.colblocks) - 1; }
 
 // row swizzle (GF(2)-linear bijection of [0, 2^K)): with the short phase on top, the rows a warp
 // touches in one access land in distinct banks in every phase (tools/bank_model.py)
@@ -590,8 +594,8 @@ k_cols(F fld0, ColKArgs<F> args) {
 
   const int c = threadIdx.x % W;
   const int t = threadIdx.x / W;
-  const int64_t inst = blockIdx.x / args.colblocks;
-  const int64_t col = (blockIdx.x - inst * args.colblocks) * W + c;
+  const int64_t inst = blockIdx.x >> cb_log(args);
+  const int64_t col = (blockIdx.x & (args.colblocks - 1)) * W + c;
   const int64_t base = inst * args.n + col;
   const int64_t m = args.m;
   const bool second = (!INV) && blockIdx.y == 1;
@@ -653,8 +657,8 @@ k_cols_fwd2(F fld0, ColKArgs<F> args) {
 
   const int c = threadIdx.x % W;
   const int t = threadIdx.x / W;
-  const int64_t inst = blockIdx.x / args.colblocks;
-  const int64_t col = (blockIdx.x - inst * args.colblocks) * W + c;
+  const int64_t inst = blockIdx.x >> cb_log(args);
+  const int64_t col = (blockIdx.x & (args.colblocks - 1)) * W + c;
   const int64_t base = inst * args.n + col;
   const int64_t m = args.m;
   const ColIdx<PH, W> idx{c};
@@ -725,8 +729,8 @@ k_cols_inv2(F fld0, ColKArgs<F> args) {
 
   const int c = threadIdx.x % W;
   const int t = threadIdx.x / W;
-  const int64_t inst = blockIdx.x / args.colblocks;     // colblocks = m / (2 W)
-  const int64_t base = inst * args.n + (blockIdx.x - inst * args.colblocks) * 2 * W + (VEC ? 2 * c : c);
+  const int64_t inst = blockIdx.x >> cb_log(args);     // colblocks = m / (2 W)
+  const int64_t base = inst * args.n + (blockIdx.x & (args.colblocks - 1)) * 2 * W + (VEC ? 2 * c : c);
   const int64_t m = args.m;
   const ColIdx<PH, W> idx{c};
   const auto fv = field_view(fld0, args, inst);
@@ -844,8 +848,8 @@ k_cols_tma(F fld0, ColKArgs<F> args, const __grid_constant__ CUtensorMap map0, c
   auto decode = [&](int64_t tile, int64_t& inst, int64_t& cb, int& second) {
     const int64_t unit = INV ? tile : (tile >> 1);
     second = INV ? 0 : (int)(tile & 1);
-    inst = unit / args.colblocks;
-    cb = unit - inst * args.colblocks;
+    inst = unit >> cb_log(args);
+    cb = unit & (args.colblocks - 1);
   };
   auto issue = [&](int64_t tile, int st) {
     int64_t inst, cb;
