@@ -218,8 +218,10 @@ static int get_plan(int dev, uint64_t p, uint64_t f, int L, cudaStream_t st, std
     bytes = 2 * n * 8;
     if (!rc) rc = upload(&dp->twf, mf.data(), n * 8, ps);
     if (!rc) rc = upload(&dp->twi, mi.data(), n * 8, ps);
-    dp->last_si64 = mulmod(dp->hp.last_si, R, p);
-    dp->last_k64 = mulmod(dp->hp.K, R, p);
+    // the leaves are Montgomery products too (a b R^-1): the final scaling undoes that R
+    const uint64_t R2 = mulmod(R, R, p);
+    dp->last_si64 = mulmod(dp->hp.last_si, R2, p);
+    dp->last_k64 = mulmod(dp->hp.K, R2, p);
   } else {
     bytes = 2 * n * 8;
     if (!rc) rc = upload(&dp->twf, dp->hp.s.data(), n * 8, ps);

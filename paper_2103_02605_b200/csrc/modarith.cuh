@@ -275,9 +275,26 @@ struct FieldGold {
     u = mulm(s, si_k);
     v = mulm(d, k);
   }
-  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mul(a, b); }
+  // x mod p for any 64-bit x: x >= p only if x_hi == 2^32 - 1 and x_lo != 0, and then x - p = (x_lo - 1, 0)
+  __device__ __forceinline__ static uint64_t canon_w(uint64_t x) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .pred p, q;\n\t"
+        "mov.u32         %0, %2;\n\t"
+        "mov.u32         %1, %3;\n\t"
+        "setp.eq.u32     p, %3, 0xffffffff;\n\t"
+        "setp.ne.and.u32 q, %2, 0, p;\n\t"
+        "@q sub.u32      %0, %2, 1;\n\t"
+        "@q mov.u32      %1, 0;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(lo32(x)), "r"(hi32(x)));
+    return mk(r0, r1);
+  }
+  // leaves (var x var): both factors are weak, so one is canonicalised first (mulm's precondition:
+  // one factor < p) and the Montgomery reduction yields a b R^-1; the plan's scaling constants
+  // carry the compensating R (api.cu: last_si and K are uploaded times R^2).
+  __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mulm(canon_w(a), b); }
   __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
-    return mulm(mul(a, b), k);
+    return mulm(leaf(a, b), k);
   }
 };
 

@@ -105,3 +105,14 @@ def test_mont_reduce_precondition_boundary():
             assert (t >> 64) <= P - 2
             r = f(*[(t >> (32 * i)) & 0xFFFFFFFF for i in range(4)])
             assert r == t * rinv % P
+
+
+def test_canon_w_any_64_bit():
+    """FieldGold::canon_w: x mod p for every 64-bit x (the leaves canonicalise one factor so that the
+    Montgomery reduction's precondition holds for two weak operands)."""
+    f = sim.helper(SRC, "canon_w")
+    rng = random.Random(8)
+    for x in EDGE + [rng.getrandbits(64) for _ in range(3000)] + [P + rng.getrandbits(32) for _ in range(500)]:
+        if x > M64:
+            continue
+        assert f(x) == x % P, hex(x)

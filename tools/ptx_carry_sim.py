@@ -133,13 +133,19 @@ def run(text: str, nout: int, inputs):
 
 def helper(src: str, fn: str):
     """Python callable on 64-bit values for FieldGold.<fn> (add_c, sub_c, sub_w) or on the four
-    product words for the reductions (reduce4, mont_reduce)."""
+    product words for the reductions (reduce4, mont_reduce), or on one 64-bit value (canon_w)."""
     text, nout, nin = extract(src, fn)
     if fn.startswith("reduce4") or fn == "mont_reduce":
         def f(t0, t1, t2, t3):
             r0, r1 = run(text, nout, [t0, t1, t2, t3])
             return r0 | (r1 << 32)
         return f
+
+    if nin == 2:   # one 64-bit operand (canon_w)
+        def h(a):
+            r0, r1 = run(text, nout, [a & M32, a >> 32])
+            return r0 | (r1 << 32)
+        return h
 
     def g(a, b):
         r0, r1 = run(text, nout, [a & M32, a >> 32, b & M32, b >> 32])
