@@ -45,8 +45,8 @@ UNIT = "Gelem/s"
 # MEASURED_PEAKS.json's copy bandwidth (driver-written).
 HBM_GBS_FALLBACK = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 # primitive kinds per element width: (R_const probe, R_var probe, IMAD.WIDE slots per modmul)
-PRIMS = {"u64": ("gold_mulm", "gold_mul", 4), "u32": ("u32_mulc", "u32_leaf", 2), "fp2": ("m31x2_mul", "m31x2_mul", 4)}
-PROBE_ITERS = {"gold_mul": 20000, "gold_mulm": 20000, "u32_mulc": 60000, "u32_leaf": 40000, "m31x2_mul": 30000, "imad_wide": 100000,
+PRIMS = {"u64": ("gold_mulm", "gold_leaf", 4), "u32": ("u32_mulc", "u32_leaf", 2), "fp2": ("m31x2_mul", "m31x2_mul", 4)}
+PROBE_ITERS = {"gold_mul": 20000, "gold_mulm": 20000, "gold_leaf": 20000, "u32_mulc": 60000, "u32_leaf": 40000, "m31x2_mul": 30000, "imad_wide": 100000,
                "gold_fwd_a": 15000, "gold_fwd_b": 15000, "gold_inv": 15000, "u32_fwd_a": 40000}
 
 WORKLOADS = {

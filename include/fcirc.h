@@ -188,7 +188,8 @@ int fcirc_profile_read(int64_t* counts, double* ms, int nkinds);
  * One warm-up and one timed launch on `stream` (CUDA events; synchronises the stream): every SM at
  * full occupancy, 8 independent dependency chains per thread, `iters` iterations per chain.
  *   kind  FCIRC_PRIM_*:
- *           GOLD_MUL    Goldilocks 64x64 -> canonical modmul, var x var (the leaves' plain reduction)
+ *           GOLD_MUL    Goldilocks 64x64 -> canonical modmul by the special reduction (2^64 = 2^32 - 1)
+ *           GOLD_LEAF   Goldilocks var x var modmul of the leaves (canonicalise one factor, then Montgomery)
  *           GOLD_MULM   Goldilocks const x var modmul (Montgomery form, R = 2^64: every twiddle product)
  *           GOLD_FWD_A / GOLD_FWD_B / GOLD_INV  the three Goldilocks butterflies (1 modmul each)
  *           U32_MULC    Shoup const x var modmul (p = 998244353)
@@ -210,6 +211,7 @@ int fcirc_profile_read(int64_t* counts, double* ms, int nkinds);
 #define FCIRC_PRIM_IMAD_WIDE 7
 #define FCIRC_PRIM_M31X2_MUL 8
 #define FCIRC_PRIM_GOLD_MULM 9
+#define FCIRC_PRIM_GOLD_LEAF 10
 int fcirc_primitive_rate(int kind, int64_t iters, double* ops_per_s, double* ms, void* stream);
 
 /* release all cached plans and trim the current device's default memory pool (tests / teardown) */

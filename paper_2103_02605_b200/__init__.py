@@ -133,7 +133,7 @@ def plan_count():
 
 PRIMITIVES = {"gold_mul": 0, "gold_fwd_a": 1, "gold_fwd_b": 2, "gold_inv": 3, "u32_mulc": 4, "u32_leaf": 5,
               "u32_fwd_a": 6, "imad_wide": 7, "m31x2_mul": 8,
-              "gold_mulm": 9}
+              "gold_mulm": 9, "gold_leaf": 10}
 
 
 def primitive_rate(kind: str, iters: int = 20000, stream=None):

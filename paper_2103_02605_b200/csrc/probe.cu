@@ -30,7 +30,7 @@ __device__ __forceinline__ uint64_t probe_seed(int c) {
 template <int KIND>
 __global__ void __launch_bounds__(kProbeThreads) k_probe(int64_t iters, uint64_t* sink) {
   uint64_t acc = 0;
-  if constexpr (KIND == FCIRC_PRIM_GOLD_MUL || KIND == FCIRC_PRIM_GOLD_MULM || KIND == FCIRC_PRIM_GOLD_FWD_A || KIND == FCIRC_PRIM_GOLD_FWD_B ||
+  if constexpr (KIND == FCIRC_PRIM_GOLD_MUL || KIND == FCIRC_PRIM_GOLD_MULM || KIND == FCIRC_PRIM_GOLD_LEAF || KIND == FCIRC_PRIM_GOLD_FWD_A || KIND == FCIRC_PRIM_GOLD_FWD_B ||
                 KIND == FCIRC_PRIM_GOLD_INV) {
     const FieldGold fld;
     uint64_t x[NCH], y[NCH];
@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(kProbeThreads) k_probe(int64_t iters, uint64_t
       for (int c = 0; c < NCH; ++c) {
         if constexpr (KIND == FCIRC_PRIM_GOLD_MUL) x[c] = FieldGold::mul(x[c], (c & 1) ? s : s2);
         else if constexpr (KIND == FCIRC_PRIM_GOLD_MULM) x[c] = FieldGold::mulm(x[c], (c & 1) ? s : s2);
+        else if constexpr (KIND == FCIRC_PRIM_GOLD_LEAF) x[c] = fld.leaf(x[c], y[c]);
         else if constexpr (KIND == FCIRC_PRIM_GOLD_FWD_A) fld.fwd_a(x[c], y[c], (c & 1) ? s : s2);
         else if constexpr (KIND == FCIRC_PRIM_GOLD_FWD_B) fld.fwd_b(x[c], y[c], (c & 1) ? s : s2);
         else fld.inv(x[c], y[c], (c & 1) ? s : s2);
@@ -152,6 +153,7 @@ extern "C" int fcirc_primitive_rate(int kind, int64_t iters, double* ops_per_s, 
     case FCIRC_PRIM_IMAD_WIDE: return probe_run<FCIRC_PRIM_IMAD_WIDE>(iters, ops_per_s, ms, st);
     case FCIRC_PRIM_M31X2_MUL: return probe_run<FCIRC_PRIM_M31X2_MUL>(iters, ops_per_s, ms, st);
     case FCIRC_PRIM_GOLD_MULM: return probe_run<FCIRC_PRIM_GOLD_MULM>(iters, ops_per_s, ms, st);
+    case FCIRC_PRIM_GOLD_LEAF: return probe_run<FCIRC_PRIM_GOLD_LEAF>(iters, ops_per_s, ms, st);
     default: return FCIRC_EINVAL;
   }
 }
