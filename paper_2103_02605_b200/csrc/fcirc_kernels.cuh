@@ -357,8 +357,7 @@ template <class F, int M> struct TwStage { static constexpr bool value = false; 
 template <int M> struct TwStage<FieldU32, M> { static constexpr bool value = M >= 6; };
 template <int M> struct TwStage<FieldU32M, M> { static constexpr bool value = M >= 6; };
 
-template <class F, int M, int R, int IPC, int MINB = 1, int EMB = EMB_PLAIN, bool TWS = false, bool SHF = false,
-          bool PF = false>
+template <class F, int M, int R, int IPC, int MINB = 1, int EMB = EMB_PLAIN, bool TWS = false, bool SHF = false>
 __global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
 k_block(F fld0, BlockKArgs<F> args) {
   pdl_entry();
@@ -412,24 +411,6 @@ k_block(F fld0, BlockKArgs<F> args) {
     else return ldtw(table + ((gbase | tb) >> (bit + 1)) + (cs >> (bit + 1)));
   };
 
-  // PF (unstaged launches): before each exchange barrier, prefetch into L1 the lines holding this
-  // thread's twiddles of every level of the NEXT phase (per level a contiguous run of <= R/2 entries
-  // from the slot-0 index), so the barrier wait and the exchange hide the L2 latency of the first
-  // twiddle loads after it (ncu: the u32 sub-problem kernel stalled on long_scoreboard at the first
-  // products of a phase)
-  auto prefetch_phase = [&](const Tw* table, int ph) {
-    if constexpr (PF && !TWS) {
-      const int rp = PH::rp(ph), lo = PH::lo(ph), tb = PH::ins_t(ph, t), cs = PH::cslot(ph, 0);
-#pragma unroll
-      for (int l = 0; l < PH::r; ++l) {
-        if (l >= rp) break;
-        const int bit = lo + rp - 1 - l;
-        const Tw* a = table + ((gbase | tb) >> (bit + 1)) + (cs >> (bit + 1));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
-      }
-    }
-  };
-
   // Work assignment: CTA b -> sub-block E = b mod 2^k and seq consecutive instance groups
   // (b >> k) seq + it, it < seq, of IPC instances each.  seq > 1 (staged launches) stages the
   // twiddle slice once per seq sub-problems (S1 k_block -14 %).  No
@@ -479,10 +460,7 @@ k_block(F fld0, BlockKArgs<F> args) {
         exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx);
       }
     } else {
-      if (ph > 0) {
-        prefetch_phase(view_twf<F>(fv, args), ph);
-        exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx);
-      }
+      if (ph > 0) exchange2<PH, R>(xa, xb, sa, sb, ph - 1, ph, t, idx);
     }
     forward_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
       const Tw tw = tw_at(view_twf<F>(fv, args), twsf, bit, tb, cs);
@@ -511,10 +489,7 @@ k_block(F fld0, BlockKArgs<F> args) {
         if (ph == NPH - 2) lane_transpose<R>(xm, t & (R - 1));
         else if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx);
       } else {
-        if (ph < NPH - 1) {
-          prefetch_phase(view_twi<F>(fv, args), ph);
-          exchange<PH, R>(xm, sa, ph + 1, ph, t, idx);
-        }
+        if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx);
       }
       inverse_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
         if (bit == M - 1 && top) fld.inv_last(xm[s0], xm[s1], view_lsi<F>(fv, args), view_lk<F>(fv, args));

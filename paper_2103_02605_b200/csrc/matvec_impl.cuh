@@ -131,20 +131,14 @@ static int launch_block_t(const F& fld, const BlockKArgs<F>& args, cudaStream_t 
   constexpr int TGT = (RR <= 8 || (sizeof(E) == 4 && !TWS && !EMB && M == 12)) ? 1024 : 512;
   constexpr int MINB = (T * IPC < TGT) ? TGT / (T * IPC) : 1;
   auto kern = k_block<F, M, R, IPC, MINB, EMB, TWS>;
-  int variant = 0;
   if constexpr (M == 12 && R == 8 && !EMB) {
     // FCIRC_SHFL=1: the last exchange of sub-problem launches as an in-warp lane transpose (A/B only;
     // measured slower)
     static const int shf = knob("SHFL", 0);
-    if (shf && args.k > 0) kern = k_block<F, M, R, IPC, MINB, EMB, TWS, true>, variant = 1;
+    if (shf && args.k > 0) kern = k_block<F, M, R, IPC, MINB, EMB, TWS, true>;
   }
-  if constexpr (M == 12 && !EMB && !TWS) {
-    // FCIRC_TWPF: L1 prefetch of the next phase's twiddle lines before each exchange barrier
-    static const int twpf = knob("TWPF", 0);
-    if (twpf && args.k > 0 && variant == 0) kern = k_block<F, M, R, IPC, MINB, EMB, TWS, false, true>, variant = 2;
-  }
-  static std::atomic<uint32_t> attr_mask[3];   // opt-in shared memory once per (kernel, device)
-  if (!smem_optin((const void*)kern, smem, attr_mask[variant]))
+  static std::atomic<uint32_t> attr_mask[2];   // opt-in shared memory once per (kernel, device)
+  if (!smem_optin((const void*)kern, smem, attr_mask[kern == k_block<F, M, R, IPC, MINB, EMB, TWS> ? 0 : 1]))
     return FCIRC_ECUDA;
   const int64_t batch = args.units >> args.k;
   BlockKArgs<F> a2 = args;
