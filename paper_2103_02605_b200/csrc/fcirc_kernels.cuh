@@ -677,9 +677,9 @@ k_cols_fwd2(F fld0, ColKArgs<F> args) {
       const uint32_t pos = (uint32_t)(col + row * m);
       xa[s] = io_load<EMB, false>(args.src0, src_inst<F>(args, inst), pos, (uint32_t)args.n, args.io);
       xb[s] = io_load<EMB, true>(args.src1, src_inst<F>(args, inst), pos, (uint32_t)args.n, args.io);
-    } else if constexpr (OFF32) {
-      xa[s] = pa[(uint32_t)row * mm];
-      xb[s] = pb[(uint32_t)row * mm];
+    } else if constexpr (OFF32) {   // global non-coherent loads (the opaque base alone gives generic LD)
+      xa[s] = __ldg(pa + (uint32_t)row * mm);
+      xb[s] = __ldg(pb + (uint32_t)row * mm);
     } else {
       xa[s] = args.src0[base + row * m];
       xb[s] = args.src1[base + row * m];
@@ -696,8 +696,8 @@ k_cols_fwd2(F fld0, ColKArgs<F> args) {
   for (int s = 0; s < R; ++s) {
     if constexpr (OFF32) {
       const uint32_t ad = (uint32_t)(PH::ins_t(NPH - 1, t) + PH::cslot(NPH - 1, s)) * mm;
-      qa[ad] = xa[s];
-      qb[ad] = xb[s];
+      __stcg(qa + ad, xa[s]);   // st.global (STG), L2 only: read back by the next pass, not this SM
+      __stcg(qb + ad, xb[s]);
     } else {
       const int64_t ad = base + (int64_t)(PH::ins_t(NPH - 1, t) + PH::cslot(NPH - 1, s)) * m;
       args.dst0[ad] = xa[s];
