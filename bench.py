@@ -59,6 +59,10 @@ WORKLOADS = {
        for L in range(12, 23) if L != 20},
     "C3": "C3: polynomial products mod 998244353, 2^20 x 2^20 coefficients -> 2^21 circulant (f=1), batch 16",
     "C5": "C5: 2^22-bit integer products, 16-bit limbs, 3 primes x 2^19 circulant (f=1) + CRT + carry, batch 8",
+    "N3_gold": ("NEXT-3 (Corollary 1): Goldilocks usual circulant matvec of order n=1000003 (not a power of two, "
+                "embedded in 2^21), batch 32"),
+    "N3_u32": ("NEXT-3 (Corollary 1): p=998244353 usual circulant matvec of order n=1000003 (not a power of two, "
+               "embedded in 2^21), batch 32"),
     **{f"S2_n{n}": (f"S2 (context): the paper's experiment, 10000 products of two {n}-coefficient polynomials in "
                     f"Z/(2^31-1)[sqrt 3] (P:110-133)") for n in (8, 16, 32, 64, 128, 256, 512)},
 }
@@ -240,12 +244,14 @@ class Workload:
         cfg = dict(synth.CONFIGS[name])
         self.kind = cfg.pop("kind")
         self.cfg = rank_config(cfg, rank)
-        if self.kind == "matvec":
+        if self.kind in ("matvec", "anyn"):
             self.inp = synth.matvec_inputs(**self.cfg)
             self.p, self.n, self.batch = self.inp["p"], self.inp["n"], self.inp["batch"]
             self.width = cfg_dtype(self.p)
             self.elems = self.batch * self.n                 # output entries
             self.mm_n, self.mm_batch = self.n, self.batch    # matvec instances launched per step
+            if self.kind == "anyn":                          # embedded in the smallest 2^m >= 2n - 1
+                self.mm_n = next_pow2(2 * self.n - 1)
         elif self.kind == "polymul":
             self.inp = synth.polymul_inputs(**self.cfg)
             self.p, self.batch = self.inp["p"], self.inp["batch"]
@@ -268,7 +274,7 @@ class Workload:
     def setup(self, torch, fc):
         self.torch, self.fc = torch, fc
         i = self.inp
-        if self.kind == "matvec":
+        if self.kind in ("matvec", "anyn"):
             self.dev = [torch.from_numpy(i["a"]).cuda(), torch.from_numpy(i["b"]).cuda()]
             self.out = torch.empty_like(self.dev[0])
         elif self.kind == "polymul":
@@ -282,6 +288,8 @@ class Workload:
         fc, (x, y) = self.fc, self.dev
         if self.kind == "matvec":
             fc.matvec(x, y, self.inp["f"], self.p, out=self.out)
+        elif self.kind == "anyn":
+            fc.circulant_matvec(x, y, self.p, out=self.out)
         elif self.kind == "polymul":
             fc.polymul(x, y, self.p, out=self.out)
         else:
@@ -298,7 +306,7 @@ class Workload:
 
     def _host_arrays(self):
         i = self.inp
-        return (i["a"], i["b"]) if self.kind in ("matvec", "polymul") else (i["x"], i["y"])
+        return (i["a"], i["b"]) if self.kind in ("matvec", "polymul", "anyn") else (i["x"], i["y"])
 
     def host_step(self):
         """One step through the public API from pinned host memory (H2D, product, D2H)."""
@@ -312,7 +320,7 @@ class Workload:
         self.host_out.copy_(self.out, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return ("pinned host -> device copies, fcirc_%s, device -> pinned host copy, synchronize"
-                % ("polymul" if self.kind == "polymul" else "bigint_mul"))
+                % {"polymul": "polymul", "anyn": "circulant_matvec"}.get(self.kind, "bigint_mul"))
 
     # ---------------------------------------------------------------- CPU oracle sample
     def cpu_sample(self, seconds: float, step_index: int = 0):
@@ -370,6 +378,9 @@ class Workload:
                "parallelism": f"replicas x{args.gpus} (independent instances per GPU, no collective)"}
         if self.kind == "matvec":
             blk["f"] = "w^n" if self.inp.get("w") not in (None, 1) else ("1" if self.inp["f"] == 1 else "p-1")
+        if self.kind == "anyn":
+            blk["f"] = "1 (usual circulant)"
+            blk["embedded_order"] = int(self.mm_n)
         return blk
 
 
@@ -425,6 +436,17 @@ def bench_parity(wl, out, thetas: int, instances: int) -> dict:
         return {"sampled_instances": int(len(ks)), "entries": r1["entries"], "eigen_instances": wl.batch,
                 "thetas_per_instance": thetas, "mismatches": r1["mismatches"] + r2["mismatches"],
                 "eigen_ok": r2["eigen_ok"], "seconds": round(time.time() - t0, 2)}
+    if wl.kind == "anyn":   # sampled entries (Definition 2, f = 1) + sum(c) = sum(a) sum(b) on every instance
+        ks = np.unique(np.linspace(0, wl.batch - 1, min(instances, wl.batch)).astype(np.int64))
+        sub = dict(i, a=i["a"][ks], b=i["b"][ks], batch=len(ks))
+        r1 = parity.check_matvec(wl.name + "[bench sampled]", sub, host[ks], full=False, thetas=0)
+        bad_sum = 0
+        for k in range(wl.batch):   # theta = 1 is an n-th root of f = 1 for every n
+            sa, sb, sc = (int(np.sum(x.astype(object))) for x in (i["a"][k], i["b"][k], host[k]))
+            bad_sum += (sc - sa * sb) % wl.p != 0
+        assert bad_sum == 0, f"{wl.name}: {bad_sum} instances fail sum(c) = sum(a) sum(b)"
+        return {"sampled_instances": int(len(ks)), "entries": r1["entries"], "sum_check_instances": wl.batch,
+                "mismatches": r1["mismatches"] + int(bad_sum), "seconds": round(time.time() - t0, 2)}
     if wl.kind == "polymul" and wl.p == synth.M31X2:   # the paper's ring: every coefficient, 4 instances
         import oracle
         ks = np.unique(np.linspace(0, wl.batch - 1, min(instances, wl.batch)).astype(np.int64))

@@ -155,6 +155,10 @@ CONFIGS = {
                         seed=BASE_SEED + 3) for L in range(12, 23)},
     "C5": dict(kind="bigint", nwords=1 << 17, batch=8, seed=BASE_SEED + 4),
     "S1": dict(kind="matvec", p=P998, n=1 << 20, batch=64, f_mode="wn", seed=BASE_SEED + 5),
+    # NEXT-3 (Corollary 1): usual circulants (f = 1) of an order that is not a power of
+    # two (n = 1000003, a prime), embedded by the library in order 2^21; batch 32
+    "N3_gold": dict(kind="anyn", p=GOLDILOCKS, n=1000003, batch=32, f_mode="one", seed=BASE_SEED + 7),
+    "N3_u32": dict(kind="anyn", p=P998, n=1000003, batch=32, f_mode="one", seed=BASE_SEED + 7),
     # S2 (context only): the paper's own experiment shape -- 10000 products of two
     # n-coefficient polynomials in its ring Z/(2^31-1)[sqrt 3], n = 8 .. 512
     **{f"S2_n{n}": dict(kind="polymul", p=M31X2, na=n, nb=n, batch=10000, seed=BASE_SEED + 6)
