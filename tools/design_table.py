@@ -7,11 +7,12 @@ import json
 import sys
 
 ORDER = ["C4n20", "C4_n12", "C4_n14", "C4_n16", "C4_n18", "C4_n22", "S1", "C2_f1", "C2_fm1", "C1", "C3", "C5",
-         "S2_n512"]
+         "S2_n512", "N3_gold", "N3_u32"]
 NAMES = {"C4n20": "**C4 n=2^20 (headline)**", "C4_n12": "C4 n=2^12", "C4_n14": "C4 n=2^14", "C4_n16": "C4 n=2^16",
          "C4_n18": "C4 n=2^18", "C4_n22": "C4 n=2^22", "S1": "S1 u32 n=2^20", "C2_f1": "C2 f=1", "C2_fm1": "C2 f=p−1",
          "C1": "C1 n=2^10, batch 1 (graph)", "C3": "C3 polymul (circulant entries)",
-         "C5": "C5 bigint (output limb positions, graph)", "S2_n512": "S2 n=512 (paper ring, its own product rate)"}
+         "C5": "C5 bigint (output limb positions, graph)", "S2_n512": "S2 n=512 (paper ring, its own product rate)",
+         "N3_gold": "N3 any-n n=1000003, Goldilocks (outputs)", "N3_u32": "N3 any-n n=1000003, u32 (outputs)"}
 
 
 def f(x, n=3):

@@ -8,7 +8,7 @@ TAG=${1:-r02}
 mkdir -p gpurun_out
 timeout 600 python bench.py > gpurun_out/bench_C4n20.json 2> gpurun_out/bench_C4n20.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-for c in S1 C2_f1 C2_fm1 C1 C3 C5 C4_n12 C4_n14 C4_n16 C4_n18 C4_n22 S2_n512; do
+for c in S1 C2_f1 C2_fm1 C1 C3 C5 C4_n12 C4_n14 C4_n16 C4_n18 C4_n22 S2_n512 N3_gold N3_u32; do
   timeout 600 python bench.py --config $c --steps 20 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
 done
 timeout 300 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-parity --no-probe > gpurun_out/plain.log 2>&1 && \
