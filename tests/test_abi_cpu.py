@@ -273,3 +273,13 @@ def test_primitive_rate_and_plan_count_validation_before_device():
     assert lib.fcirc_primitive_rate(0, 10, None, None, None) == -1
     n, pinned = fc.plan_count()
     assert n >= 0 and 0 <= pinned <= n
+
+
+def test_binding_primitive_kinds_match_header():
+    """The binding's primitive-kind names map to exactly the FCIRC_PRIM_* values include/fcirc.h
+    declares (bench.py's R_const / R_var probes go through these names)."""
+    import re
+    import paper_2103_02605_b200 as fc
+    hdr = open(os.path.join(ROOT, "include", "fcirc.h")).read()
+    decl = {m.group(1).lower(): int(m.group(2)) for m in re.finditer(r"#define FCIRC_PRIM_(\w+) (\d+)", hdr)}
+    assert decl == fc.PRIMITIVES
