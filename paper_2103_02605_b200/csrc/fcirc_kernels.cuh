@@ -308,6 +308,27 @@ __device__ __forceinline__ void inverse_phase(int ph, int t, BF bf) {
   }
 }
 
+// The leaf products of a sub-problem.  Fields whose column-pass b butterfly stores its second
+// output negated (F::NEG_B, FieldGold::fwd_bn) hand sub-block E a b side times (-1)^popcount(E):
+// a CTA-uniform sign, undone by taking the leaves with the opposite sign (a uniform branch).
+// NEGL: the sub-problem instantiation of such a field (k > 0); the fused whole-product launch
+// (k = 0, E = 0) keeps the branch-free leaves (C4 n = 2^12 -0.8 % with the branch compiled in,
+// profiles/r02t_ab_negb.txt).
+template <class F, int R, bool NEGL, class T>
+__device__ __forceinline__ void leaves(const F& fld, T (&xm)[R], const T (&xa)[R], const T (&xb)[R], int E) {
+  if constexpr (NEGL) {
+    if (__popc(E) & 1) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) xm[s] = fld.leaf_neg(xa[s], xb[s]);
+      return;
+    }
+  } else {
+    (void)E;
+  }
+#pragma unroll
+  for (int s = 0; s < R; ++s) xm[s] = fld.leaf(xa[s], xb[s]);
+}
+
 // Instance base pointer as an opaque value: element accesses p[off] with a 32-bit row offset then
 // compile to one IMAD.WIDE.U32 (off * sizeof(T) + p) instead of a re-associated 64-bit index
 // computation (shift, add, add-with-carry).  Used where it measured faster: the Goldilocks forward
@@ -357,7 +378,8 @@ template <class F, int M> struct TwStage { static constexpr bool value = false; 
 template <int M> struct TwStage<FieldU32, M> { static constexpr bool value = M >= 6; };
 template <int M> struct TwStage<FieldU32M, M> { static constexpr bool value = M >= 6; };
 
-template <class F, int M, int R, int IPC, int MINB = 1, int EMB = EMB_PLAIN, bool TWS = false, bool SHF = false>
+template <class F, int M, int R, int IPC, int MINB = 1, int EMB = EMB_PLAIN, bool TWS = false, bool SHF = false,
+          bool NEGL = false>
 __global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
 k_block(F fld0, BlockKArgs<F> args) {
   pdl_entry();
@@ -478,8 +500,7 @@ k_block(F fld0, BlockKArgs<F> args) {
     }
   } else {
     T xm[R];
-#pragma unroll
-    for (int s = 0; s < R; ++s) xm[s] = fld.leaf(xa[s], xb[s]);
+    leaves<F, R, NEGL>(fld, xm, xa, xb, E);
 
     // ---- inverse levels (recombination c1 = (M1+M2)/(2s), c2 = (M1-M2)/2), low bits first
     const bool top = (k == 0);
@@ -620,7 +641,7 @@ k_cols(F fld0, ColKArgs<F> args) {
   if constexpr (!INV) {
     col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
       const Tw tw = col_tw<K>(view_twf<F>(fv, args), bit, tb, cs);
-      if (second) fld.fwd_b(x[s0], x[s1], tw);
+      if (second) fld.fwd_bn(x[s0], x[s1], tw);
       else fld.fwd_a(x[s0], x[s1], tw);
     });
   } else {
@@ -688,7 +709,7 @@ k_cols_fwd2(F fld0, ColKArgs<F> args) {
   col_forward<PH, K, R, NPH>(xa, &xb, sma, smb, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
     const Tw tw = col_tw<K>(view_twf<F>(fv, args), bit, tb, cs);
     fld.fwd_a(xa[s0], xa[s1], tw);
-    fld.fwd_b(xb[s0], xb[s1], tw);
+    fld.fwd_bn(xb[s0], xb[s1], tw);
   });
   T* qa = opaque(args.dst0 + base);
   T* qb = opaque(args.dst1 + base);
@@ -894,7 +915,7 @@ k_cols_tma(F fld0, ColKArgs<F> args, const __grid_constant__ CUtensorMap map0, c
     if constexpr (!INV) {
       col_forward<PH, K, R, NPH>(x, (T(*)[R]) nullptr, sm, sm, t, idx, [&](int s0, int s1, int bit, int tb, int cs) {
         const Tw tw = col_tw<K>(view_twf<F>(fv, args), bit, tb, cs);
-        if (second) fld.fwd_b(x[s0], x[s1], tw);
+        if (second) fld.fwd_bn(x[s0], x[s1], tw);
         else fld.fwd_a(x[s0], x[s1], tw);
       });
     } else {
@@ -1014,8 +1035,7 @@ k_block_pipe(F fld0, BlockKArgs<F> args) {
       });
     }
     T xm[R];
-#pragma unroll
-    for (int s = 0; s < R; ++s) xm[s] = fld.leaf(xa[s], xb[s]);
+    leaves<F, R, F::NEG_B>(fld, xm, xa, xb, E);
 #pragma unroll
     for (int ph = NPH - 1; ph >= 0; --ph) {
       if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx, hsync);

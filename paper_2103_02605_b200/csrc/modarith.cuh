@@ -67,6 +67,8 @@ struct FieldU32 {
     x = X + t;
     y = X - t + p2;
   }
+  static constexpr bool NEG_B = false;   // see FieldGold::fwd_bn
+  __device__ __forceinline__ void fwd_bn(uint32_t& x, uint32_t& y, TwU32 s) const { fwd_b(x, y, s); }
   __device__ __forceinline__ void fwd_b(uint32_t& x, uint32_t& y, TwU32 s) const {
     uint32_t t = mulc(x, s);
     uint32_t Y = red2(y);
@@ -238,6 +240,23 @@ struct FieldGold {
         : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
     return mk(r0, r1);
   }
+  // -(T 2^-64) mod p, canonical, same precondition: the subtraction's operands swapped, m - x, again
+  // a value in (-p, p) that a borrow corrects by + p
+  __device__ __forceinline__ static uint64_t mont_reduce_neg(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3) {
+    uint32_t r0, r1;
+    asm("{\n\t.reg .u32 a1, x0, x1, m;\n\t"
+        "add.cc.u32  a1, %3, %2;\n\t"     // a1 = t0 + t1, CF = e
+        "addc.cc.u32 x0, %4, a1;\n\t"     // x = xh + a1 + e
+        "addc.u32    x1, %5, 0;\n\t"
+        "sub.cc.u32  %0, %2, x0;\n\t"     // r = m - x, m = (t0, a1)
+        "subc.cc.u32 %1, a1, x1;\n\t"
+        "subc.u32    m, 0, 0;\n\t"        // m = -borrow
+        "sub.cc.u32  %0, %0, m;\n\t"      // on a borrow: r - EPS = r + p (mod 2^64)
+        "subc.u32    %1, %1, 0;\n\t"
+        "}"
+        : "=&r"(r0), "=&r"(r1) : "r"(t0), "r"(t1), "r"(t2), "r"(t3));
+    return mk(r0, r1);
+  }
   // x * s mod p, canonical, for any 64-bit x and a table constant sR = s R mod p (< p)
   __device__ __forceinline__ static uint64_t mulm(uint64_t x, uint64_t sR) {
     const uint64_t lo = x * sR, hi = __umul64hi(x, sR);
@@ -260,6 +279,21 @@ struct FieldGold {
     const uint64_t Y = y;
     x = add_c(Y, t);
     y = sub_w(t, Y);
+  }
+  // forward b of the column passes (the top K levels of a multi-pass product): the second output is
+  // stored NEGATED, y - t instead of t - y: with a weak y, t - y needs two borrow corrections (sub_w,
+  // 8 instructions) and y - t one (sub_c, 5).  The split is linear, so the whole lower sub-block and
+  // everything computed from it carries the factor -1, again at every column level: the b side of
+  // sub-block E (the row of the column, its bits the path through the K levels) is times
+  // (-1)^popcount(E) when the sub-problem kernel reads it, uniformly for a CTA, which takes its
+  // leaf products with the opposite sign then (leaf_neg: the operands of the Montgomery
+  // reduction's subtraction swapped, no extra instruction).  NEG_B marks the fields that do this.
+  static constexpr bool NEG_B = true;
+  __device__ __forceinline__ void fwd_bn(uint64_t& x, uint64_t& y, uint64_t s) const {
+    const uint64_t t = mulm(x, s);
+    const uint64_t Y = y;
+    x = add_c(Y, t);
+    y = sub_c(Y, t);
   }
   // inverse: inputs canonical (leaf products and inverse outputs are canonical); outputs canonical.
   // (add_c and mul use the predicated corrections, like the forward butterflies.)
@@ -293,6 +327,12 @@ struct FieldGold {
   // one factor < p) and the Montgomery reduction yields a b R^-1; the plan's scaling constants
   // carry the compensating R (api.cu: last_si and K are uploaded times R^2).
   __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mulm(canon_w(a), b); }
+  // -(a b R^-1): the leaf of a sub-block whose b side arrives negated (fwd_bn)
+  __device__ __forceinline__ uint64_t leaf_neg(uint64_t a, uint64_t b) const {
+    const uint64_t x = canon_w(a);
+    const uint64_t lo = x * b, hi = __umul64hi(x, b);
+    return mont_reduce_neg(lo32(lo), hi32(lo), lo32(hi), hi32(hi));
+  }
   __device__ __forceinline__ uint64_t single(uint64_t a, uint64_t b, uint64_t k) const {
     return mulm(leaf(a, b), k);
   }
@@ -338,6 +378,8 @@ struct FieldM31x2 {
     x = add(X, t);
     y = sub(X, t);
   }
+  static constexpr bool NEG_B = false;   // see FieldGold::fwd_bn
+  __device__ __forceinline__ void fwd_bn(uint64_t& x, uint64_t& y, uint64_t s) const { fwd_b(x, y, s); }
   __device__ __forceinline__ void fwd_b(uint64_t& x, uint64_t& y, uint64_t s) const {
     const uint64_t t = mul(x, s);
     const uint64_t Y = y;

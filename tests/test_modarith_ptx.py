@@ -95,6 +95,57 @@ def test_mont_reduce_const_times_var(seed):
             assert r == t * rinv % P, (hex(x), hex(s), hex(r))
 
 
+@pytest.mark.parametrize("seed", [16, 17])
+def test_mont_reduce_neg_is_the_negated_reduction(seed):
+    """FieldGold::mont_reduce_neg (the leaves of a sub-block whose b side arrives negated from the
+    column passes): -(T * 2^-64) mod p, canonical, under mont_reduce's precondition."""
+    f = sim.helper(SRC, "mont_reduce_neg")
+    rng = random.Random(seed)
+    rinv = pow(1 << 64, -1, P)
+    xs = EDGE + [rng.getrandbits(64) for _ in range(1500)] + [M64 - rng.getrandbits(33) for _ in range(500)]
+    ss = [0, 1, 2, P - 1, P - 2, 0xFFFFFFFF, 1 << 32, (1 << 32) + 1, 0x8000000000000000, 0xFFFFFFFF00000000,
+          (1 << 32) - 1 + (1 << 63)] + [rng.randrange(P) for _ in range(40)] + [P - 1 - rng.getrandbits(33) for _ in range(20)]
+    for x in xs:
+        for s in ss:
+            t = x * s
+            r = f(*[(t >> (32 * i)) & 0xFFFFFFFF for i in range(4)])
+            assert r == (-t * rinv) % P, (hex(x), hex(s), hex(r))
+
+
+def test_forward_b_negated_lower_half_gives_popcount_signs():
+    """The column passes' b butterfly (FieldGold::fwd_bn) stores y - s x for s x - y.  By linearity the
+    in-place forward split of b then leaves position i of the instance times (-1)^popcount(i') where
+    i' are the address bits of the negating levels: checked on a small Python model of the in-place
+    split over Z/p with the top K of L levels negating (the kernels' schedule: K column levels,
+    then the sub-problem kernel with the plain butterfly and the sign (-1)^popcount(E) at its leaves)."""
+    rng = random.Random(5)
+    L, K = 6, 3
+    n = 1 << L
+    w = rng.randrange(2, P)
+    # any heap table works for the sign argument (linearity only): random twiddles per (level, block)
+    tw = {(d, e): rng.randrange(1, P) for d in range(L) for e in range(1 << d)}
+    b = [rng.randrange(P) for _ in range(n)]
+
+    def split(neg_levels):
+        x = list(b)
+        for d in range(L):
+            h = n >> (d + 1)
+            for e in range(1 << d):
+                s = tw[(d, e)]
+                for j in range(h):
+                    i0, i1 = e * 2 * h + j, e * 2 * h + j + h
+                    t = s * x[i0] % P
+                    lo = (t - x[i1]) % P
+                    x[i0], x[i1] = (t + x[i1]) % P, ((-lo) % P if d < neg_levels else lo)
+        return x
+    plain, negk = split(0), split(K)
+    for i in range(n):
+        E = i >> (L - K)
+        sign = -1 if bin(E).count("1") & 1 else 1
+        assert negk[i] == (sign * plain[i]) % P, i
+    del w
+
+
 def test_mont_reduce_precondition_boundary():
     """The largest high word the reduction admits is p - 2 (x = 2^64 - 1, s = p - 1): still exact."""
     f = sim.helper(SRC, "mont_reduce")

@@ -135,7 +135,7 @@ def helper(src: str, fn: str):
     """Python callable on 64-bit values for FieldGold.<fn> (add_c, sub_c, sub_w) or on the four
     product words for the reductions (reduce4, mont_reduce), or on one 64-bit value (canon_w)."""
     text, nout, nin = extract(src, fn)
-    if fn.startswith("reduce4") or fn == "mont_reduce":
+    if fn.startswith("reduce4") or fn.startswith("mont_reduce"):
         def f(t0, t1, t2, t3):
             r0, r1 = run(text, nout, [t0, t1, t2, t3])
             return r0 | (r1 << 32)
