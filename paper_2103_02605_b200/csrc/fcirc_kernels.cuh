@@ -308,25 +308,47 @@ __device__ __forceinline__ void inverse_phase(int ph, int t, BF bf) {
   }
 }
 
-// The leaf products of a sub-problem.  Fields whose column-pass b butterfly stores its second
-// output negated (F::NEG_B, FieldGold::fwd_bn) hand sub-block E a b side times (-1)^popcount(E):
-// a CTA-uniform sign, undone by taking the leaves with the opposite sign (a uniform branch).
-// NEGL: the sub-problem instantiation of such a field (k > 0); the fused whole-product launch
-// (k = 0, E = 0) keeps the branch-free leaves (C4 n = 2^12 -0.8 % with the branch compiled in,
-// profiles/r02t_ab_negb.txt).
-template <class F, int R, bool NEGL, class T>
-__device__ __forceinline__ void leaves(const F& fld, T (&xm)[R], const T (&xa)[R], const T (&xb)[R], int E) {
-  if constexpr (NEGL) {
-    if (__popc(E) & 1) {
+// Sign-tracking vector split (fields with F::NEG_B, FieldGold).  The b butterfly's second output
+// s x - y is a canonical-minus-weak subtraction (two borrow corrections); its negative y - s x needs
+// one (fwd_bn).  A level that stores the negative multiplies, by linearity, everything below the
+// lower child by -1, so the b leaf at address x of sub-block E arrives times
+// (-1)^(popcount(E) + popcount(x & NEGMASK)), NEGMASK the address bits of the negating levels of the
+// sub-problem (all K column levels negate: popcount(E)).  The leaf product takes that sign back
+// (leaf_neg: the operands of the Montgomery reduction's final subtraction swapped, same instruction
+// count).  Negating are the levels whose sign costs nothing at the leaves, where address = t << r | slot:
+//   * bits [0, r): slot bits -- the sign is a compile-time property of the slot;
+//   * bits >= r + 5: thread bits >= 5 -- the sign is uniform over a warp (with E: one non-divergent branch);
+// the five levels in between (lane bits) keep the plain butterfly (their sign would differ per lane:
+// the conditional negations cost what those levels save, profiles/r02t_ab_negb_hyb_pred.txt).
+template <class PH>
+__host__ __device__ constexpr int neg_mask() {
+  constexpr int RL = PH::rp(PH::NPH - 1);
+  return ((1 << RL) - 1) | ~((1 << (RL + 5)) - 1);
+}
+template <class PH, class F>
+__host__ __device__ constexpr bool neg_level(int bit) {
+  if constexpr (F::NEG_B) return (neg_mask<PH>() >> bit) & 1;
+  else return false;
+}
+template <class PH, class F, int R, class T>
+__device__ __forceinline__ void leaves(const F& fld, T (&xm)[R], const T (&xa)[R], const T (&xb)[R], int E, int t) {
+  if constexpr (F::NEG_B) {
+    constexpr int L = PH::NPH - 1;
+    static_assert(PH::lo(L) == 0, "leaf layout: address = t << r | slot");
+    if ((__popc(E) + __popc(t >> 5)) & 1) {   // warp-uniform
 #pragma unroll
-      for (int s = 0; s < R; ++s) xm[s] = fld.leaf_neg(xa[s], xb[s]);
-      return;
+      for (int s = 0; s < R; ++s)
+        xm[s] = (__builtin_popcount(PH::cslot(L, s) & neg_mask<PH>()) & 1) ? fld.leaf(xa[s], xb[s]) : fld.leaf_neg(xa[s], xb[s]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < R; ++s)
+        xm[s] = (__builtin_popcount(PH::cslot(L, s) & neg_mask<PH>()) & 1) ? fld.leaf_neg(xa[s], xb[s]) : fld.leaf(xa[s], xb[s]);
     }
   } else {
-    (void)E;
-  }
+    (void)E; (void)t;
 #pragma unroll
-  for (int s = 0; s < R; ++s) xm[s] = fld.leaf(xa[s], xb[s]);
+    for (int s = 0; s < R; ++s) xm[s] = fld.leaf(xa[s], xb[s]);
+  }
 }
 
 // Instance base pointer as an opaque value: element accesses p[off] with a 32-bit row offset then
@@ -378,8 +400,7 @@ template <class F, int M> struct TwStage { static constexpr bool value = false; 
 template <int M> struct TwStage<FieldU32, M> { static constexpr bool value = M >= 6; };
 template <int M> struct TwStage<FieldU32M, M> { static constexpr bool value = M >= 6; };
 
-template <class F, int M, int R, int IPC, int MINB = 1, int EMB = EMB_PLAIN, bool TWS = false, bool SHF = false,
-          bool NEGL = false>
+template <class F, int M, int R, int IPC, int MINB = 1, int EMB = EMB_PLAIN, bool TWS = false, bool SHF = false>
 __global__ void __launch_bounds__((1 << M) / R * IPC, MINB)
 k_block(F fld0, BlockKArgs<F> args) {
   pdl_entry();
@@ -487,7 +508,8 @@ k_block(F fld0, BlockKArgs<F> args) {
     forward_phase<PH, R>(ph, t, [&](int s0, int s1, int bit, int tb, int cs) {
       const Tw tw = tw_at(view_twf<F>(fv, args), twsf, bit, tb, cs);
       fld.fwd_a(xa[s0], xa[s1], tw);
-      fld.fwd_b(xb[s0], xb[s1], tw);
+      if (neg_level<PH, F>(bit)) fld.fwd_bn(xb[s0], xb[s1], tw);   // compile-time after unrolling
+      else fld.fwd_b(xb[s0], xb[s1], tw);
     });
   }
 
@@ -500,7 +522,7 @@ k_block(F fld0, BlockKArgs<F> args) {
     }
   } else {
     T xm[R];
-    leaves<F, R, NEGL>(fld, xm, xa, xb, E);
+    leaves<PH, F, R>(fld, xm, xa, xb, E, t);
 
     // ---- inverse levels (recombination c1 = (M1+M2)/(2s), c2 = (M1-M2)/2), low bits first
     const bool top = (k == 0);
@@ -1035,7 +1057,7 @@ k_block_pipe(F fld0, BlockKArgs<F> args) {
       });
     }
     T xm[R];
-    leaves<F, R, F::NEG_B>(fld, xm, xa, xb, E);
+    leaves<PH, F, R>(fld, xm, xa, xb, E, t);
 #pragma unroll
     for (int ph = NPH - 1; ph >= 0; --ph) {
       if (ph < NPH - 1) exchange<PH, R>(xm, sa, ph + 1, ph, t, idx, hsync);

@@ -132,21 +132,13 @@ static int launch_block_t(const F& fld, const BlockKArgs<F>& args, cudaStream_t 
   constexpr int MINB = (T * IPC < TGT) ? TGT / (T * IPC) : 1;
   auto kern = k_block<F, M, R, IPC, MINB, EMB, TWS>;
   int variant = 0;
-  // fields whose column passes hand over a signed b side (F::NEG_B): sub-problem launches take the
-  // instantiation with the signed leaves (launches with k > 0 are never embedded)
-  constexpr bool NEGL = F::NEG_B && !EMB;
-  if constexpr (NEGL) {
-    if (args.k > 0) { kern = k_block<F, M, R, IPC, MINB, EMB, TWS, false, true>; variant = 1; }
-  } else if (F::NEG_B && args.k > 0) {
-    return FCIRC_EINVAL;
-  }
   if constexpr (M == 12 && R == 8 && !EMB) {
     // FCIRC_SHFL=1: the last exchange of sub-problem launches as an in-warp lane transpose (A/B only;
     // measured slower)
     static const int shf = knob("SHFL", 0);
-    if (shf && args.k > 0) { kern = k_block<F, M, R, IPC, MINB, EMB, TWS, true, NEGL>; variant = 2; }
+    if (shf && args.k > 0) { kern = k_block<F, M, R, IPC, MINB, EMB, TWS, true>; variant = 1; }
   }
-  static std::atomic<uint32_t> attr_mask[3];   // opt-in shared memory once per (kernel, device)
+  static std::atomic<uint32_t> attr_mask[2];   // opt-in shared memory once per (kernel, device)
   if (!smem_optin((const void*)kern, smem, attr_mask[variant]))
     return FCIRC_ECUDA;
   const int64_t batch = args.units >> args.k;

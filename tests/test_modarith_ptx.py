@@ -112,38 +112,38 @@ def test_mont_reduce_neg_is_the_negated_reduction(seed):
             assert r == (-t * rinv) % P, (hex(x), hex(s), hex(r))
 
 
-def test_forward_b_negated_lower_half_gives_popcount_signs():
-    """The column passes' b butterfly (FieldGold::fwd_bn) stores y - s x for s x - y.  By linearity the
-    in-place forward split of b then leaves position i of the instance times (-1)^popcount(i') where
-    i' are the address bits of the negating levels: checked on a small Python model of the in-place
-    split over Z/p with the top K of L levels negating (the kernels' schedule: K column levels,
-    then the sub-problem kernel with the plain butterfly and the sign (-1)^popcount(E) at its leaves)."""
-    rng = random.Random(5)
-    L, K = 6, 3
-    n = 1 << L
-    w = rng.randrange(2, P)
-    # any heap table works for the sign argument (linearity only): random twiddles per (level, block)
+@pytest.mark.parametrize("L,K,mask", [(6, 3, 0), (7, 2, 0b10011), (8, 0, 0b11000111), (5, 2, 0b111)])
+def test_forward_b_negating_levels_give_popcount_signs(L, K, mask):
+    """The b butterfly of a negating level (FieldGold::fwd_bn) stores y - s x for s x - y.  By linearity the
+    in-place forward split of b then leaves position i of the instance times
+    (-1)^(popcount(E) + popcount(x & mask)), i = E 2^M + x, when all K column levels negate and so do
+    the sub-problem levels whose pair bit is in `mask` (the kernels' rule, fcirc_kernels.cuh neg_mask:
+    slot bits and warp-uniform thread bits of the leaf layout): checked on a Python model of the
+    in-place split over Z/p with random twiddles (the sign argument uses linearity only)."""
+    rng = random.Random(5 + L)
+    n, M = 1 << L, L - K
     tw = {(d, e): rng.randrange(1, P) for d in range(L) for e in range(1 << d)}
     b = [rng.randrange(P) for _ in range(n)]
 
-    def split(neg_levels):
+    def split(negating):
         x = list(b)
         for d in range(L):
-            h = n >> (d + 1)
+            h = n >> (d + 1)          # pair bit of level d: log2(h) = L - 1 - d
             for e in range(1 << d):
                 s = tw[(d, e)]
                 for j in range(h):
                     i0, i1 = e * 2 * h + j, e * 2 * h + j + h
                     t = s * x[i0] % P
                     lo = (t - x[i1]) % P
-                    x[i0], x[i1] = (t + x[i1]) % P, ((-lo) % P if d < neg_levels else lo)
+                    x[i0], x[i1] = (t + x[i1]) % P, ((-lo) % P if negating(d) else lo)
         return x
-    plain, negk = split(0), split(K)
+    plain = split(lambda d: False)
+    # column levels d < K always negate; sub-problem level d >= K has pair bit L - 1 - d < M
+    signed = split(lambda d: d < K or (mask >> (L - 1 - d)) & 1)
     for i in range(n):
-        E = i >> (L - K)
-        sign = -1 if bin(E).count("1") & 1 else 1
-        assert negk[i] == (sign * plain[i]) % P, i
-    del w
+        E, x = i >> M, i & ((1 << M) - 1)
+        par = bin(E).count("1") + bin(x & mask).count("1")
+        assert signed[i] == ((-1) ** par * plain[i]) % P, i
 
 
 def test_mont_reduce_precondition_boundary():
