@@ -402,6 +402,42 @@ except fc.FcircError as e:
     assert "rejected -1" in out.stdout, out.stdout + out.stderr
 
 
+@pytest.mark.parametrize("knobs", [
+    {"FCIRC_GOLD_RB": "4", "FCIRC_GOLD_RBF": "4"},
+    {"FCIRC_GOLD_RB": "16", "FCIRC_GOLD_RBF": "16"},
+    {"FCIRC_GOLD_MSPLIT": "11"},
+    {"FCIRC_GOLD_MSPLIT": "13"},
+    {"FCIRC_SMALL_R": "8"},
+    {"FCIRC_SHFL": "1"},
+    {"FCIRC_COLS2": "0", "FCIRC_INV2": "0", "FCIRC_TMA": "0"},
+])
+def test_goldilocks_launcher_variants_all_entries(knobs):
+    """The Goldilocks kernels under the launcher's run-time knobs (other register blockings R, on-chip
+    sub-problem sizes 2^11 / 2^13, the lane-transpose exchange, the one-operand column passes): every
+    entry against Definition 2.  The sign-tracking vector split derives its
+    negating levels from the phase layout, which differs per (M, R): each variant is a separate
+    instantiation of the rule.  Knobs are read once per process, hence the subprocess."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, oracle, paper_2103_02605_b200 as fc, synth
+p = synth.GOLDILOCKS
+bad = []
+for L, batch in [(3, 5), (9, 3), (10, 2), (11, 3), (12, 3), (13, 2), (14, 2), (15, 1)]:
+    inp = synth.matvec_inputs(p, 1 << L, batch, seed=900 + L)
+    c = fc.matvec(torch.from_numpy(inp["a"]).cuda(), torch.from_numpy(inp["b"]).cuda(), inp["f"], p).cpu().numpy()
+    for k in range(batch):
+        exp = oracle.fcirc_entries(p, inp["f"], inp["a"][k], inp["b"][k])
+        if not np.array_equal(c[k].astype(np.uint64), exp):
+            bad.append((L, k))
+print("mismatching (L, instance):", bad)
+'''
+    env = dict(os.environ, **knobs)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert "mismatching (L, instance): []" in out.stdout, out.stdout + out.stderr[-2000:]
+
+
 @pytest.mark.parametrize("p", [P998, GOLDILOCKS])
 def test_circulant_any_n_corollary1(p):
     """fcirc_circulant_matvec (Corollary 1, P:102-107): usual circulant of any order n, every entry
