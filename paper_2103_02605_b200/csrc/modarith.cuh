@@ -282,14 +282,13 @@ struct FieldGold {
     x = add_c(Y, t);
     y = sub_w(t, Y);
   }
-  // forward b of the column passes (the top K levels of a multi-pass product): the second output is
-  // stored NEGATED, y - t instead of t - y: with a weak y, t - y needs two borrow corrections (sub_w,
-  // 8 instructions) and y - t one (sub_c, 5).  The split is linear, so the whole lower sub-block and
-  // everything computed from it carries the factor -1, again at every column level: the b side of
-  // sub-block E (the row of the column, its bits the path through the K levels) is times
-  // (-1)^popcount(E) when the sub-problem kernel reads it, uniformly for a CTA, which takes its
-  // leaf products with the opposite sign then (leaf_neg: the operands of the Montgomery
-  // reduction's subtraction swapped, no extra instruction).  NEG_B marks the fields that do this.
+  // forward b of a NEGATING level (sign-tracking vector split, fcirc_kernels.cuh `leaves` / neg_mask
+  // and DESIGN.md section 9): the second output is stored negated, y - t instead of t - y -- with a
+  // weak y, t - y needs two borrow corrections (sub_w, 8 instructions) and y - t one (sub_c, 5).  The
+  // split is linear, so everything computed from the lower child carries the factor -1; the leaf
+  // products take the accumulated sign back (leaf_neg: the operands of the Montgomery reduction's
+  // final subtraction swapped, no extra instruction).  Negating are all column levels and the
+  // sub-problem levels whose sign is free at the leaves.  NEG_B marks the fields that do this.
   static constexpr bool NEG_B = true;
   __device__ __forceinline__ void fwd_bn(uint64_t& x, uint64_t& y, uint64_t s) const {
     const uint64_t t = mulm(x, s);
@@ -329,7 +328,7 @@ struct FieldGold {
   // one factor < p) and the Montgomery reduction yields a b R^-1; the plan's scaling constants
   // carry the compensating R (api.cu: last_si and K are uploaded times R^2).
   __device__ __forceinline__ uint64_t leaf(uint64_t a, uint64_t b) const { return mulm(canon_w(a), b); }
-  // -(a b R^-1): the leaf of a sub-block whose b side arrives negated (fwd_bn)
+  // -(a b R^-1): the leaf at a position whose b side arrives negated (fwd_bn)
   __device__ __forceinline__ uint64_t leaf_neg(uint64_t a, uint64_t b) const {
     const uint64_t x = canon_w(a);
     const uint64_t lo = x * b, hi = __umul64hi(x, b);
